@@ -1,0 +1,144 @@
+/*
+ * b2conv — C ABI of the B200-native convolution hot path.
+ *
+ * This header is the drop-in boundary.  In the reference (cuclgen, pure Python)
+ * the device boundary is the call
+ *
+ *     backend.run_kernel(ir, launch, buffers, meta, engine, thread_order)
+ *         -> (buffers, CostReport)                      cuclgen/backend.py:1104-1133
+ *
+ * made from runner.execute_node (cuclgen/runner.py:73-106, the call at :103)
+ * and from runner.run_graph (runner.py:228).  Its arguments are a kernel IR
+ * produced by a Variant generator (variants.py:201-220) for one conv node
+ * described by ConvParams (frontend.py:56-65) on an input DimsSpec
+ * img:chan:y:x (ndarray.py:74-88), plus caller-owned buffers keyed
+ * in/filts/bias/out (runner.py:32-36).  The output buffer is written in place.
+ *
+ * Here the same call is a plain C function over device pointers: the op is a
+ * b2c_conv_desc, the variant + TuneParams are a b2c_tune, and the CostReport's
+ * wall_ns becomes CUDA-event device time (b2c_conv_time).  All tensors are
+ * fp32, dense row-major, canonical layouts: x NCHW (img:chan:y:x), w OIHW
+ * (out_chan:in_chan:y:x), bias (out_chan), y NCHW.  No torch types cross this
+ * boundary; the Python host mirror (paper_1611_06945_b200/backend.py) binds it
+ * with ctypes, and INTEGRATION.md shows the binding a maintainer of the
+ * reference would add.
+ *
+ * Error convention (mirrors cuclgen's exception families):
+ *   B2C_OK            0  success
+ *   B2C_INAPPLICABLE  1  variant cannot run this op      (variants.Inapplicable, variants.py:31)
+ *   B2C_BAD_ARGS      2  inconsistent descriptor/buffers  (oracle.ShapeMismatch, oracle.py:19;
+ *                                                          frontend.GraphError, frontend.py:47)
+ *   B2C_CUDA_ERROR    3  CUDA runtime / launch failure    (backend.InterpError family, backend.py:61-82)
+ *   B2C_UNSUPPORTED   4  precision/feature not built      (CuclgenError, errors.py:1-2)
+ * b2c_last_error() returns a thread-local message for the last failing call.
+ *
+ * Threading: every entry point is re-entrant; launches go to the stream given.
+ * The only global state is a mutex-protected per-device attribute cache and
+ * the split-K semaphore pool inside caller-provided workspace.
+ */
+#ifndef B2CONV_H
+#define B2CONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2C_OK 0
+#define B2C_INAPPLICABLE 1
+#define B2C_BAD_ARGS 2
+#define B2C_CUDA_ERROR 3
+#define B2C_UNSUPPORTED 4
+
+/* Variant ids.  The first four carry the reference's variant names
+ * (VARIANTS, variants.py:830-832; ranks at :227, :283, :333, :388);
+ * B2C_VAR_UMMA is the B200 tensor-core implicit GEMM. */
+#define B2C_VAR_SIMPLE 0 /* "conv_simple": one thread per output, fmaf over ic,ky,kx  (variants.py:223-276) */
+#define B2C_VAR_TILED 1  /* "conv_tiled" : register/thread-blocked FFMA implicit GEMM (variants.py:376-685) */
+#define B2C_VAR_1X1 2    /* "conv_1x1"   : k=1,pad=0 tcgen05 GEMM                     (variants.py:279-325) */
+#define B2C_VAR_FC 3     /* "conv_fc"    : whole-image filter, weight-streaming GEMM  (variants.py:328-373) */
+#define B2C_VAR_UMMA 4   /* "conv_umma"  : tcgen05/TMEM 3xTF32 implicit GEMM, k x k      (new, B200)       */
+
+/* Precision modes. */
+#define B2C_PREC_FP32 0 /* fp32-exact: FFMA, or 3xTF32 split on the tensor cores */
+#define B2C_PREC_BF16 1 /* bf16 operands, fp32 accumulate (separately stated tolerance) */
+
+/* One convolution, the C form of (ConvParams, input DimsSpec, fused_activation):
+ * ConvParams(ksz, stride, pad, out_chans) frontend.py:56-65; output extent
+ * window_out frontend.py:441-442; OpNode.fused_activation frontend.py:100. */
+typedef struct b2c_conv_desc {
+    int32_t n, c, h, w; /* input img:chan:y:x */
+    int32_t k;          /* out_chans */
+    int32_t r;          /* ksz (square) */
+    int32_t stride, pad;
+    int32_t oh, ow; /* must equal (h + 2*pad - r)/stride + 1 (and same for w) */
+    int32_t act;    /* 0 none, 1 relu ("(ov > 0) ? ov : 0", variants.py:164) */
+    int32_t prec;   /* B2C_PREC_* */
+} b2c_conv_desc;
+
+/* Variant + tuning knobs, the C form of TuneParams (variants.py:39-91).
+ * FFMA variants read mnt/mnb/kb/vw with the reference's meaning (register
+ * block, thread block, k unroll, vector width).  The tcgen05 variants read
+ * tile_n (MMA N), stages, split_k and swap_ab (0: M = output pixels, N =
+ * out_chans; 1: M = out_chans, N = output pixels). */
+typedef struct b2c_tune {
+    int32_t variant;
+    int32_t mnt0, mnt1, mnb0, mnb1, kb, vw;
+    int32_t tile_n, stages, split_k, swap_ab;
+} b2c_tune;
+
+/* 0 when `tune` can run `d`; otherwise B2C_INAPPLICABLE / B2C_BAD_ARGS with a
+ * reason copied into reason[0..n) (Variant.applies, variants.py:206-210). */
+int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, size_t n);
+
+/* Device workspace bytes b2c_conv_fwd needs (split-K partials + semaphores).
+ * The workspace must be zero-filled once before first use (semaphores reset
+ * themselves after every launch). */
+size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t);
+
+/* y = act(conv(x, w) + bias), written in place into caller-allocated y
+ * (run_kernel semantics, backend.py:1104-1133).  `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Asynchronous: errors from the kernel
+ * itself surface on the next synchronising call. */
+int b2c_conv_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w,
+                 const float* bias, float* y, void* workspace, size_t ws_bytes, void* stream);
+
+/* CostReport.wall_ns analogue (backend.py:108, :1125-1132): launches the
+ * variant `warmup` times, then times `reps` launches with CUDA events, each
+ * optionally preceded by an L2 flush (l2_flush != 0), and returns the median
+ * per-launch milliseconds.  Synchronises the stream. */
+int b2c_conv_time(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w,
+                  const float* bias, float* y, void* workspace, size_t ws_bytes, void* stream,
+                  int warmup, int reps, int l2_flush, float* median_ms);
+
+/* End-to-end call over HOST buffers: copies x, w, bias host->device, runs the
+ * variant, copies y device->host, all on `stream`, using device scratch the
+ * caller provides (dev_scratch of scratch_bytes >= b2c_conv_host_scratch()).
+ * This is execute_node (runner.py:73-106) with host NdArrays in and out. */
+size_t b2c_conv_host_scratch(const b2c_conv_desc* d, const b2c_tune* t);
+int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx, const float* hw,
+                      const float* hbias, float* hy, void* dev_scratch, size_t scratch_bytes,
+                      void* stream);
+
+/* FLOPs the reference counts for this op: 2*k^2*ic*oc*oy*ox*b
+ * (frontend.flops_of, frontend.py:499-514). */
+int64_t b2c_conv_flops(const b2c_conv_desc* d);
+
+/* Compulsory HBM bytes: 4*(|x| + |w| + |bias| + |y|). */
+int64_t b2c_conv_bytes(const b2c_conv_desc* d);
+
+/* Number of kernel launches one b2c_conv_fwd issues for this (d, t). */
+int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t);
+
+/* Thread-local message for the last non-zero status. */
+const char* b2c_last_error(void);
+
+/* Library version string ("b2conv <semver> sm_100a"). */
+const char* b2c_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2CONV_H */

@@ -1,0 +1,431 @@
+// b2conv C ABI: descriptor validation, variant applicability, dispatch,
+// workspace sizing, CUDA-event timing and the host-buffer end-to-end call.
+// See include/b2conv.h for the contract and the reference call it replaces
+// (cuclgen/backend.py:1104-1133 run_kernel, via runner.execute_node
+// runner.py:73-106).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/b2conv.h"
+#include "common.cuh"
+#include "k_ffma.cuh"
+#include "k_umma.cuh"
+
+using namespace b2c;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(B2C_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define B2C_CUDA(call)                                     \
+    do {                                                   \
+        cudaError_t _e = (call);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+int window_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
+
+int check_desc(const b2c_conv_desc* d) {
+    if (!d) return fail(B2C_BAD_ARGS, "null descriptor");
+    if (d->n < 1 || d->c < 1 || d->h < 1 || d->w < 1 || d->k < 1 || d->r < 1 || d->stride < 1 || d->pad < 0)
+        return fail(B2C_BAD_ARGS, "bad conv params (need n,c,h,w,k,ksz,stride >= 1, pad >= 0)");
+    const int oh = window_out(d->h, d->r, d->stride, d->pad);
+    const int ow = window_out(d->w, d->r, d->stride, d->pad);
+    if (oh < 1 || ow < 1) return fail(B2C_BAD_ARGS, "non-positive output dims");
+    if (oh != d->oh || ow != d->ow)
+        return fail(B2C_BAD_ARGS, "output extent inconsistent with params (window_out)");
+    if (d->act != 0 && d->act != 1) return fail(B2C_BAD_ARGS, "act must be 0 (none) or 1 (relu)");
+    const long long xin = (long long)d->n * d->c * d->h * d->w;
+    const long long yout = (long long)d->n * d->k * oh * ow;
+    const long long wk = (long long)d->k * d->c * d->r * d->r;
+    if (xin >= (1ll << 31) || yout >= (1ll << 31) || wk >= (1ll << 31))
+        return fail(B2C_UNSUPPORTED, "tensor exceeds 2^31 elements");
+    if (d->prec != B2C_PREC_FP32) return fail(B2C_UNSUPPORTED, "only prec=fp32 is built in this library");
+    return B2C_OK;
+}
+
+Geom make_geom(const b2c_conv_desc* d) {
+    Geom g;
+    g.N = d->n; g.C = d->c; g.H = d->h; g.W = d->w;
+    g.OC = d->k; g.R = d->r; g.S = d->stride; g.P = d->pad;
+    g.OH = d->oh; g.OW = d->ow;
+    g.K = d->c * d->r * d->r;
+    g.PQ = d->oh * d->ow;
+    g.M = d->n * g.PQ;
+    g.HW = d->h * d->w;
+    g.RR = d->r * d->r;
+    g.act = d->act;
+    g.fPQ = FastDiv((uint32_t)g.PQ);
+    g.fOW = FastDiv((uint32_t)g.OW);
+    g.fRR = FastDiv((uint32_t)g.RR);
+    g.fR = FastDiv((uint32_t)g.R);
+    return g;
+}
+
+bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || bn == 192 || bn == 256; }
+
+int is_pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; }
+
+// ----------------------------------------------------------------------------- applicability
+
+int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
+    int rc = check_desc(d);
+    if (rc) { why = g_last_error; return rc; }
+    if (!t) { why = "null tune"; return B2C_BAD_ARGS; }
+    const long long M = (long long)d->n * d->oh * d->ow;
+    switch (t->variant) {
+        case B2C_VAR_SIMPLE:
+            return B2C_OK;
+        case B2C_VAR_TILED: {
+            if (!is_pow2_in(t->mnt0, 1, 8) || !is_pow2_in(t->mnt1, 1, 8)) {
+                why = "MNt entries must be 1, 2, 4 or 8"; return B2C_INAPPLICABLE;
+            }
+            if (t->mnb0 < 1 || t->mnb1 < 1 || t->kb < 1) { why = "bad tune params"; return B2C_BAD_ARGS; }
+            const int threads = t->mnb0 * t->mnb1;
+            if (threads > 1024) { why = "workgroup exceeds 1024 threads"; return B2C_INAPPLICABLE; }
+            if (t->vw != 1 && t->vw != 2 && t->vw != 4 && t->vw != 8) { why = "vector width must be 1,2,4,8"; return B2C_BAD_ARGS; }
+            if (t->mnt1 % t->vw) { why = "vector width must divide register block"; return B2C_BAD_ARGS; }
+            // Reference applicability (variants.py:391-403).
+            if (M < t->mnt0) { why = "fewer output pixels than the register block"; return B2C_INAPPLICABLE; }
+            if (d->k < t->mnt1) { why = "fewer output channels than the register block"; return B2C_INAPPLICABLE; }
+            if (t->vw > 4) { why = "vector width 8 is not offered"; return B2C_INAPPLICABLE; }
+            const size_t sm = tiled_smem_bytes(t->mnb0 * t->mnt0, t->mnb1 * t->mnt1, t->kb);
+            if (sm > 200 * 1024) { why = "shared-memory tile too large"; return B2C_INAPPLICABLE; }
+            return B2C_OK;
+        }
+        case B2C_VAR_1X1:
+            if (d->r != 1) { why = "kernel size != 1"; return B2C_INAPPLICABLE; }
+            if (d->pad != 0) { why = "padding not supported"; return B2C_INAPPLICABLE; }
+            break;
+        case B2C_VAR_FC:
+            if (!(d->r == d->h && d->r == d->w && d->pad == 0 && d->oh == 1 && d->ow == 1)) {
+                why = "filters must cover the whole input with 1x1 output"; return B2C_INAPPLICABLE;
+            }
+            break;
+        case B2C_VAR_UMMA:
+            break;
+        default:
+            why = "unknown variant";
+            return B2C_BAD_ARGS;
+    }
+    // tcgen05 family
+    if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192,256"; return B2C_INAPPLICABLE; }
+    if (t->split_k < 1) { why = "split_k must be >= 1"; return B2C_BAD_ARGS; }
+    if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
+    const int K = d->c * d->r * d->r;
+    const int kblocks = (K + UMMA_BK - 1) / UMMA_BK;
+    if (t->split_k > kblocks) { why = "split_k exceeds the number of 32-wide K blocks"; return B2C_INAPPLICABLE; }
+    return B2C_OK;
+}
+
+// ----------------------------------------------------------------------------- launch plans
+
+struct UmmaPlan {
+    int grid_x, grid_y, split, kps, kblocks, tiles;
+    size_t ws_bytes;  // partials + semaphores
+};
+
+UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
+    UmmaPlan p;
+    const int K = d->c * d->r * d->r;
+    const int M = d->n * d->oh * d->ow;
+    const int BN = t->tile_n;
+    const int pix_tile = t->swap_ab ? BN : UMMA_M;
+    const int oc_tile = t->swap_ab ? UMMA_M : BN;
+    p.grid_x = (M + pix_tile - 1) / pix_tile;
+    p.grid_y = (d->k + oc_tile - 1) / oc_tile;
+    p.tiles = p.grid_x * p.grid_y;
+    p.kblocks = (K + UMMA_BK - 1) / UMMA_BK;
+    const int want = std::max(1, std::min(t->split_k, p.kblocks));
+    p.kps = (p.kblocks + want - 1) / want;
+    p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
+    p.ws_bytes = 0;
+    if (p.split > 1) {
+        p.ws_bytes = (size_t)p.tiles * p.split * BN * UMMA_M * sizeof(float);
+        p.ws_bytes = (p.ws_bytes + 255) & ~(size_t)255;
+        p.ws_bytes += (size_t)p.tiles * sizeof(int);
+    }
+    return p;
+}
+
+using UmmaKernel = void (*)(UmmaArgs);
+
+template <int BN, bool SWAP, int KMODE>
+int umma_smem() { return UmmaCfg<BN>::SMEM; }
+
+struct UmmaEntry {
+    UmmaKernel fn;
+    int smem;
+};
+
+template <int BN, bool SWAP, int KMODE>
+UmmaEntry umma_entry() {
+    return UmmaEntry{&k_umma<BN, SWAP, KMODE>, UmmaCfg<BN>::SMEM};
+}
+
+template <bool SWAP, int KMODE>
+UmmaEntry umma_pick_bn(int bn) {
+    switch (bn) {
+        case 32: return umma_entry<32, SWAP, KMODE>();
+        case 64: return umma_entry<64, SWAP, KMODE>();
+        case 96: return umma_entry<96, SWAP, KMODE>();
+        case 128: return umma_entry<128, SWAP, KMODE>();
+        case 192: return umma_entry<192, SWAP, KMODE>();
+        case 256: return umma_entry<256, SWAP, KMODE>();
+    }
+    return UmmaEntry{nullptr, 0};
+}
+
+UmmaEntry umma_pick(int bn, int swap, int kmode) {
+    if (swap) {
+        if (kmode == 0) return umma_pick_bn<true, 0>(bn);
+        if (kmode == 1) return umma_pick_bn<true, 1>(bn);
+        return umma_pick_bn<true, 2>(bn);
+    }
+    if (kmode == 0) return umma_pick_bn<false, 0>(bn);
+    if (kmode == 1) return umma_pick_bn<false, 1>(bn);
+    return umma_pick_bn<false, 2>(bn);
+}
+
+int kmode_of(int variant) { return variant == B2C_VAR_1X1 ? 1 : variant == B2C_VAR_FC ? 2 : 0; }
+
+// Per-device "max dynamic smem" attribute is set once per kernel.
+std::mutex g_attr_mu;
+std::vector<std::pair<const void*, int>> g_attr_done;  // (fn, device)
+
+int ensure_smem_attr(const void* fn, int bytes) {
+    int dev = 0;
+    B2C_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto& e : g_attr_done)
+        if (e.first == fn && e.second == dev) return B2C_OK;
+    B2C_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    g_attr_done.emplace_back(fn, dev);
+    return B2C_OK;
+}
+
+using TiledKernel = void (*)(Geom, const float*, const float*, const float*, float*, int, int, int);
+
+TiledKernel tiled_pick(int mt, int nt) {
+#define B2C_T(a, b) \
+    if (mt == a && nt == b) return &k_tiled<a, b>;
+    B2C_T(1, 1) B2C_T(1, 2) B2C_T(1, 4) B2C_T(1, 8)
+    B2C_T(2, 1) B2C_T(2, 2) B2C_T(2, 4) B2C_T(2, 8)
+    B2C_T(4, 1) B2C_T(4, 2) B2C_T(4, 4) B2C_T(4, 8)
+    B2C_T(8, 1) B2C_T(8, 2) B2C_T(8, 4) B2C_T(8, 8)
+#undef B2C_T
+    return nullptr;
+}
+
+int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias,
+             float* y, void* ws, size_t ws_bytes, cudaStream_t st) {
+    std::string why;
+    int rc = applies_impl(d, t, why);
+    if (rc) return fail(rc, why);
+    if (!x || !w || !bias || !y) return fail(B2C_BAD_ARGS, "null tensor pointer");
+    const Geom g = make_geom(d);
+    switch (t->variant) {
+        case B2C_VAR_SIMPLE: {
+            const long long total = (long long)g.N * g.OC * g.PQ;
+            const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 64);
+            k_simple<<<blocks, 256, 0, st>>>(g, x, w, bias, y);
+            break;
+        }
+        case B2C_VAR_TILED: {
+            TiledKernel fn = tiled_pick(t->mnt0, t->mnt1);
+            if (!fn) return fail(B2C_INAPPLICABLE, "no kernel for this register block");
+            const int BM = t->mnb0 * t->mnt0, BN = t->mnb1 * t->mnt1;
+            const size_t sm = tiled_smem_bytes(BM, BN, t->kb);
+            rc = ensure_smem_attr((const void*)fn, (int)sm);
+            if (rc) return rc;
+            dim3 grid((g.M + BM - 1) / BM, (g.OC + BN - 1) / BN);
+            fn<<<grid, t->mnb0 * t->mnb1, sm, st>>>(g, x, w, bias, y, t->mnb0, t->mnb1, t->kb);
+            break;
+        }
+        default: {
+            const UmmaPlan p = umma_plan(d, t);
+            UmmaEntry e = umma_pick(t->tile_n, t->swap_ab, kmode_of(t->variant));
+            if (!e.fn) return fail(B2C_INAPPLICABLE, "no tcgen05 kernel for this tile");
+            if (p.split > 1 && (!ws || ws_bytes < p.ws_bytes))
+                return fail(B2C_BAD_ARGS, "workspace too small for split-K (see b2c_conv_workspace)");
+            rc = ensure_smem_attr((const void*)e.fn, e.smem);
+            if (rc) return rc;
+            UmmaArgs a;
+            a.g = g;
+            a.x = x; a.w = w; a.bias = bias; a.y = y;
+            a.split = p.split; a.kps = p.kps; a.kblocks = p.kblocks;
+            a.ws = reinterpret_cast<float*>(ws);
+            a.sems = nullptr;
+            if (p.split > 1) {
+                const size_t part = ((size_t)p.tiles * p.split * t->tile_n * UMMA_M * sizeof(float) + 255) & ~(size_t)255;
+                a.sems = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + part);
+            }
+            dim3 grid(p.grid_x, p.grid_y, p.split);
+            e.fn<<<grid, UMMA_THREADS, e.smem, st>>>(a);
+            break;
+        }
+    }
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) return cuda_fail(le, "kernel launch");
+    return B2C_OK;
+}
+
+// L2 flush buffer (one per device), larger than the 126 MB L2.
+std::mutex g_flush_mu;
+std::vector<std::pair<int, void*>> g_flush;
+constexpr size_t kFlushBytes = 256ull << 20;
+
+int flush_l2(cudaStream_t st) {
+    int dev = 0;
+    B2C_CUDA(cudaGetDevice(&dev));
+    void* buf = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_flush_mu);
+        for (auto& e : g_flush)
+            if (e.first == dev) buf = e.second;
+        if (!buf) {
+            B2C_CUDA(cudaMalloc(&buf, kFlushBytes));
+            g_flush.emplace_back(dev, buf);
+        }
+    }
+    B2C_CUDA(cudaMemsetAsync(buf, 0, kFlushBytes, st));
+    return B2C_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, size_t n) {
+    std::string why;
+    const int rc = applies_impl(d, t, why);
+    if (reason && n) {
+        std::snprintf(reason, n, "%s", rc ? why.c_str() : "");
+    }
+    if (rc) g_last_error = why;
+    return rc;
+}
+
+size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t) {
+    std::string why;
+    if (applies_impl(d, t, why)) return 0;
+    if (t->variant == B2C_VAR_SIMPLE || t->variant == B2C_VAR_TILED) return 0;
+    return umma_plan(d, t).ws_bytes;
+}
+
+int b2c_conv_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias,
+                 float* y, void* workspace, size_t ws_bytes, void* stream) {
+    return fwd_impl(d, t, x, w, bias, y, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b2c_conv_time(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias,
+                  float* y, void* workspace, size_t ws_bytes, void* stream, int warmup, int reps, int l2_flush,
+                  float* median_ms) {
+    if (!median_ms || reps < 1 || warmup < 0) return fail(B2C_BAD_ARGS, "bad timing arguments");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    for (int i = 0; i < warmup; ++i) {
+        int rc = fwd_impl(d, t, x, w, bias, y, workspace, ws_bytes, st);
+        if (rc) return rc;
+    }
+    std::vector<float> ms(reps);
+    cudaEvent_t e0, e1;
+    B2C_CUDA(cudaEventCreate(&e0));
+    B2C_CUDA(cudaEventCreate(&e1));
+    int rc = B2C_OK;
+    for (int i = 0; i < reps && rc == B2C_OK; ++i) {
+        if (l2_flush) rc = flush_l2(st);
+        if (rc) break;
+        cudaEventRecord(e0, st);
+        rc = fwd_impl(d, t, x, w, bias, y, workspace, ws_bytes, st);
+        cudaEventRecord(e1, st);
+        if (rc) break;
+        cudaError_t se = cudaEventSynchronize(e1);
+        if (se != cudaSuccess) { rc = cuda_fail(se, "cudaEventSynchronize"); break; }
+        cudaEventElapsedTime(&ms[i], e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    std::sort(ms.begin(), ms.end());
+    *median_ms = ms[reps / 2];
+    return B2C_OK;
+}
+
+size_t b2c_conv_host_scratch(const b2c_conv_desc* d, const b2c_tune* t) {
+    if (check_desc(d)) return 0;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t xb = (size_t)d->n * d->c * d->h * d->w * 4;
+    const size_t wb = (size_t)d->k * d->c * d->r * d->r * 4;
+    const size_t bb = (size_t)d->k * 4;
+    const size_t yb = (size_t)d->n * d->k * d->oh * d->ow * 4;
+    return al(xb) + al(wb) + al(bb) + al(yb) + al(b2c_conv_workspace(d, t));
+}
+
+int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx, const float* hw,
+                      const float* hbias, float* hy, void* dev_scratch, size_t scratch_bytes, void* stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (!hx || !hw || !hbias || !hy || !dev_scratch) return fail(B2C_BAD_ARGS, "null pointer");
+    const size_t need = b2c_conv_host_scratch(d, t);
+    if (scratch_bytes < need) return fail(B2C_BAD_ARGS, "device scratch too small (b2c_conv_host_scratch)");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t xb = (size_t)d->n * d->c * d->h * d->w * 4;
+    const size_t wb = (size_t)d->k * d->c * d->r * d->r * 4;
+    const size_t bb = (size_t)d->k * 4;
+    const size_t yb = (size_t)d->n * d->k * d->oh * d->ow * 4;
+    char* p = reinterpret_cast<char*>(dev_scratch);
+    float* dx = reinterpret_cast<float*>(p); p += al(xb);
+    float* dw = reinterpret_cast<float*>(p); p += al(wb);
+    float* db = reinterpret_cast<float*>(p); p += al(bb);
+    float* dy = reinterpret_cast<float*>(p); p += al(yb);
+    void* ws = p;
+    const size_t wsb = b2c_conv_workspace(d, t);
+    B2C_CUDA(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, st));
+    B2C_CUDA(cudaMemcpyAsync(dw, hw, wb, cudaMemcpyHostToDevice, st));
+    B2C_CUDA(cudaMemcpyAsync(db, hbias, bb, cudaMemcpyHostToDevice, st));
+    rc = fwd_impl(d, t, dx, dw, db, dy, ws, wsb, st);
+    if (rc) return rc;
+    B2C_CUDA(cudaMemcpyAsync(hy, dy, yb, cudaMemcpyDeviceToHost, st));
+    return B2C_OK;
+}
+
+int64_t b2c_conv_flops(const b2c_conv_desc* d) {
+    if (!d) return 0;
+    return 2ll * d->r * d->r * d->c * d->k * d->oh * d->ow * d->n;
+}
+
+int64_t b2c_conv_bytes(const b2c_conv_desc* d) {
+    if (!d) return 0;
+    return 4ll * ((int64_t)d->n * d->c * d->h * d->w + (int64_t)d->k * d->c * d->r * d->r + d->k +
+                  (int64_t)d->n * d->k * d->oh * d->ow);
+}
+
+int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
+    (void)d;
+    (void)t;
+    return 1;
+}
+
+const char* b2c_last_error(void) { return g_last_error.c_str(); }
+
+const char* b2c_version(void) { return "b2conv 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""Execution harness: run one conv op through libb2conv.
+
+Mirrors the single-op part of cuclgen/runner.py: ``node_test_inputs``
+(runner.py:39-45, with the seeded-noise recipe of oracle.py:48-60),
+``conv_reduction_terms`` (:66-70) and ``execute_node`` (:73-106) — canonical
+NdArrays in, canonical NdArray + CostReport out, output written into a
+caller-shaped buffer.  The kernel runs on the B200 through the C ABI; the
+CostReport's ``wall_ns`` is the kernel's CUDA-event time.
+
+``ConvOp`` is the device-resident form used by the tuner and the bench: the
+operands live in HBM and ``launch()`` issues exactly one kernel on the
+current stream (so it can be captured in a CUDA graph).
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import backend
+from .backend import CostReport
+from .errors import CuclgenError
+from .frontend import KIND_CONV, OpNode
+from .ndarray import NdArray, nda_from_np
+from .variants import STATIC, KernelPlan, TuneParams, Variant, conv_shape
+
+
+def seed_for(signature: str) -> int:
+    """Process-independent 64-bit seed: first 8 bytes (LE) of sha256 (oracle.py:48-50)."""
+    return int.from_bytes(hashlib.sha256(signature.encode()).digest()[:8], "little")
+
+
+def noise(names, sizes, seed: int, low: float = 0.1, high: float = 1.0) -> NdArray:
+    """Uniform fp32 synthetic data; [0.1, 1) is the reference recipe (oracle.py:53-60)."""
+    n = int(np.prod(sizes, dtype=np.int64))
+    vals = np.random.default_rng(seed).uniform(low, high, size=n).astype(np.float32)
+    return nda_from_np(names, vals.reshape(tuple(sizes)))
+
+
+def node_test_inputs(node: OpNode, edges, seed, low: float = 0.1, high: float = 1.0) -> dict:
+    """Seeded noise for every input edge of a node, seed ``f"{seed}:{edge}"`` (runner.py:39-45)."""
+    return {e: noise(edges[e].names, edges[e].sizes, seed_for(f"{seed}:{e}"), low, high) for e in node.inputs}
+
+
+def conv_reduction_terms(node: OpNode, edges) -> int:
+    """ic*k*k, the reduction length that picks the tolerance (runner.py:66-70)."""
+    if node.kind != KIND_CONV:
+        return 1
+    return edges[node.inputs[0]].size_of("chan") * node.params.ksz ** 2
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        from .errors import DeviceError
+
+        raise DeviceError("no CUDA device: the B200 conv path has no CPU fallback")
+    return torch
+
+
+class ConvOp:
+    """One conv bound to device operands and a kernel plan; ``launch()`` = one kernel."""
+
+    def __init__(self, plan: KernelPlan, x, w, bias, y=None, device=None):
+        torch = _torch()
+        self.plan = plan
+        d = plan.desc
+        dev = device or x.device
+        for t, shape in ((x, (d.n, d.c, d.h, d.w)), (w, (d.k, d.c, d.r, d.r)), (bias, (d.k,))):
+            if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+                raise CuclgenError(f"operand {tuple(t.shape)} {t.dtype} does not match {shape} fp32 contiguous CUDA")
+        self.x, self.w, self.bias = x, w, bias
+        self.y = y if y is not None else torch.empty((d.n, d.k, d.oh, d.ow), dtype=torch.float32, device=dev)
+        self.ws = backend.alloc_workspace(d, plan.tune, device=dev)
+
+    @property
+    def flops(self) -> int:
+        return backend.conv_flops(self.plan.desc)
+
+    @property
+    def bytes(self) -> int:
+        return backend.conv_bytes(self.plan.desc)
+
+    def launch(self, stream=None):
+        backend.fwd(self.plan.desc, self.plan.tune, self.x, self.w, self.bias, self.y, self.ws, stream)
+
+    def time_ms(self, warmup=3, reps=10, l2_flush=True) -> float:
+        return backend.time_ms(self.plan.desc, self.plan.tune, self.x, self.w, self.bias, self.y, self.ws,
+                               warmup, reps, l2_flush)
+
+
+def to_device(nda: NdArray, device="cuda"):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(nda.to_np())).to(device)
+
+
+def execute_node(node: OpNode, edges, inputs: dict, variant: Variant, params: TuneParams | None = None,
+                 mode: str = STATIC, engine=None, thread_order=None, inst: KernelPlan | None = None, src=None):
+    """Run one node's kernel on canonical inputs; returns (canonical output NdArray,
+    CostReport) like runner.execute_node (runner.py:73-106).  ``engine`` /
+    ``thread_order`` / ``src`` belong to the reference's simulator and are
+    accepted for signature compatibility only."""
+    torch = _torch()
+    if params is None:
+        params = variant.default_params(node, edges)
+    plan = inst if inst is not None else variant.generate(node, edges, params, mode)
+    x, w, b = (to_device(inputs[e]) for e in node.inputs)
+    op = ConvOp(plan, x, w, b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    op.launch()
+    e1.record()
+    e1.synchronize()
+    out_spec = edges[node.outputs[0]]
+    got = op.y.cpu().numpy().reshape(out_spec.sizes)
+    return nda_from_np(out_spec.names, got), CostReport(wall_ns=int(e0.elapsed_time(e1) * 1e6))
+
+
+@dataclass
+class HostRun:
+    """Pinned host operands + device scratch for the end-to-end call
+    (b2c_conv_fwd_host: H2D inputs, kernel, D2H output on one stream)."""
+
+    plan: KernelPlan
+    hx: object
+    hw: object
+    hb: object
+    hy: object
+    scratch: object
+
+    @staticmethod
+    def create(plan: KernelPlan, x_np, w_np, b_np, device="cuda") -> "HostRun":
+        torch = _torch()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).pin_memory()  # noqa: E731
+        d = plan.desc
+        hy = torch.empty((d.n, d.k, d.oh, d.ow), dtype=torch.float32).pin_memory()
+        nbytes = backend.lib().b2c_conv_host_scratch(backend.ctypes.byref(d), backend.ctypes.byref(plan.tune))
+        scratch = torch.zeros(int(nbytes), dtype=torch.uint8, device=device)
+        return HostRun(plan, pin(x_np), pin(w_np), pin(b_np), hy, scratch)
+
+    @property
+    def h2d_bytes(self) -> int:
+        return 4 * (self.hx.numel() + self.hw.numel() + self.hb.numel())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return 4 * self.hy.numel()
+
+    def run(self, stream=None):
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        L = backend.lib()
+        rc = L.b2c_conv_fwd_host(backend.ctypes.byref(self.plan.desc), backend.ctypes.byref(self.plan.tune),
+                                 self.hx.data_ptr(), self.hw.data_ptr(), self.hb.data_ptr(), self.hy.data_ptr(),
+                                 self.scratch.data_ptr(), self.scratch.numel(), st)
+        backend.check(rc, "b2c_conv_fwd_host")
+
+
+def shape_of(node: OpNode, edges):
+    return conv_shape(node, edges)

@@ -1,0 +1,296 @@
+"""Conv variants and their tuning parameters — the reference's variant API on B200.
+
+Mirrors cuclgen/variants.py: ``TuneParams`` (variants.py:39-91) with the same
+string form, the ``Variant`` protocol (``applies`` / ``required_formats`` /
+``generate`` / ``tune_candidates``, variants.py:201-220), the ``VARIANTS``
+registry (:830-832), ``variants_for_kind`` (:835-837) and ``select_variant``
+(:840-856: a TuneDB record wins, else the most specialized applicable variant).
+
+What changes is what ``generate`` produces.  The reference emits CUCL kernel
+text for its SIMT interpreter; here a variant resolves to one of the
+hand-written sm_100a kernels in libb2conv.so and ``generate`` returns the
+launch plan (C descriptor + tune struct) the C ABI executes:
+
+    conv_simple  one thread per output, exact fmaf order     (variants.py:223-276)
+    conv_tiled   FFMA register/thread-blocked implicit GEMM  (variants.py:376-685)
+    conv_umma    tcgen05/TMEM 3xTF32 implicit GEMM, k x k     (new)
+    conv_1x1     tcgen05 GEMM for k=1, pad=0                 (variants.py:279-325)
+    conv_fc      tcgen05 weight-streaming GEMM, k = h = w     (variants.py:328-373)
+
+Every kernel reads canonical NCHW / OIHW and writes NCHW, so
+``required_formats`` is canonical for all of them (no conversion passes,
+unlike ConvTiled's padded NHWC output, variants.py:416-424).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import backend
+from .errors import CuclgenError, Inapplicable
+from .frontend import KIND_CONV, OpNode
+
+STATIC = "static"
+DYNAMIC = "dynamic"
+
+UMMA_BN = (32, 64, 96, 128, 192, 256)
+NUM_SMS = 148
+
+
+@dataclass(frozen=True)
+class TuneParams:
+    """The reference knobs (MNt register block, MNb thread block, Kb reduction
+    chunk, vw vector width, lf/li staging flags) plus the tcgen05 knobs:
+    bn (MMA N tile), split_k, swap_ab (M = out_chans instead of pixels)."""
+
+    mnt: tuple = (4, 4)
+    mnb: tuple = (16, 16)
+    kb: int = 4
+    vw: int = 4
+    use_local_filts: bool = True
+    use_local_in: bool = True
+    bn: int = 128
+    split_k: int = 1
+    swap_ab: bool = False
+
+    def __post_init__(self):
+        if min(self.mnt) < 1 or min(self.mnb) < 1 or self.kb < 1:
+            raise CuclgenError(f"bad tune params {self}")
+        if self.threads > 1024:
+            raise CuclgenError(f"workgroup of {self.threads} threads exceeds 1024")
+        if self.vw not in (1, 2, 4, 8):
+            raise CuclgenError(f"vector width must be one of 1,2,4,8, got {self.vw}")
+        if self.mnt[1] % self.vw:
+            raise CuclgenError(f"vector width {self.vw} must divide register block {self.mnt[1]}")
+        if self.bn < 1 or self.split_k < 1:
+            raise CuclgenError(f"bad tcgen05 tile params {self}")
+
+    @property
+    def threads(self) -> int:
+        return self.mnb[0] * self.mnb[1]
+
+    def to_string(self) -> str:
+        return (f"MNt={self.mnt[0]}:{self.mnt[1]},MNb={self.mnb[0]}:{self.mnb[1]},Kb={self.kb},vw={self.vw},"
+                f"lf={int(self.use_local_filts)},li={int(self.use_local_in)},"
+                f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)}")
+
+    @staticmethod
+    def from_string(text: str) -> "TuneParams":
+        """Parses the reference form (variants.py:73-91); the tcgen05 keys are optional."""
+        kv = dict(part.partition("=")[::2] for part in text.split(","))
+        try:
+            return TuneParams(
+                mnt=tuple(int(v) for v in kv["MNt"].split(":")),
+                mnb=tuple(int(v) for v in kv["MNb"].split(":")),
+                kb=int(kv["Kb"]),
+                vw=int(kv["vw"]),
+                use_local_filts=kv.get("lf", "1") == "1",
+                use_local_in=kv.get("li", "1") == "1",
+                bn=int(kv.get("BN", "128")),
+                split_k=int(kv.get("sk", "1")),
+                swap_ab=kv.get("sw", "0") == "1",
+            )
+        except (KeyError, ValueError) as e:
+            raise CuclgenError(f"bad tune-params string {text!r}: {e}") from None
+
+
+DEFAULT_TUNE = TuneParams()
+
+
+@dataclass(frozen=True)
+class VariantFormats:
+    """Operand layouts a variant requires; empty/None = canonical (graphopt.py:89-94)."""
+
+    inputs: dict = field(default_factory=dict)
+    output: object = None
+
+
+@dataclass(frozen=True)
+class ConvShape:
+    b: int
+    ic: int
+    h: int
+    w: int
+    oc: int
+    oy: int
+    ox: int
+    ksz: int
+    stride: int
+    pad: int
+
+    @property
+    def m(self) -> int:
+        return self.b * self.oy * self.ox
+
+    @property
+    def k(self) -> int:
+        return self.ic * self.ksz * self.ksz
+
+
+def conv_shape(node: OpNode, edges) -> ConvShape:
+    ind, outd = edges[node.inputs[0]], edges[node.outputs[0]]
+    if ind is None or outd is None:
+        raise CuclgenError(f"node '{node.name}': shapes not inferred")
+    p = node.params
+    b, ic, h, w = (ind.size_of(d) for d in ("img", "chan", "y", "x"))
+    return ConvShape(b, ic, h, w, outd.size_of("chan"), outd.size_of("y"), outd.size_of("x"), p.ksz, p.stride, p.pad)
+
+
+def conv_desc(node: OpNode, edges, prec: int = backend.PREC_FP32) -> backend.ConvDesc:
+    s = conv_shape(node, edges)
+    act = node.fused_activation
+    if act not in (None, "relu"):
+        raise Inapplicable(f"no fused form for activation '{act}'")
+    return backend.make_desc(s.b, s.ic, s.h, s.w, s.oc, s.ksz, s.stride, s.pad, s.oy, s.ox, act == "relu", prec)
+
+
+@dataclass(frozen=True)
+class KernelPlan:
+    """What ``generate`` returns: the C launch description of one op."""
+
+    variant: str
+    desc: backend.ConvDesc
+    tune: backend.Tune
+    params: TuneParams
+
+    @property
+    def name(self) -> str:
+        d = self.desc
+        return f"{self.variant}_b{d.n}_ic{d.c}_y{d.h}_x{d.w}_oc{d.k}_k{d.r}_s{d.stride}_p{d.pad}"
+
+
+class Variant:
+    name: str
+    rank: int
+    kind: str = KIND_CONV
+    vid: int
+
+    def tune_struct(self, params: TuneParams) -> backend.Tune:
+        return backend.Tune(self.vid, params.mnt[0], params.mnt[1], params.mnb[0], params.mnb[1], params.kb,
+                            params.vw, params.bn, 0, params.split_k, int(params.swap_ab))
+
+    def applies(self, node: OpNode, edges, params: TuneParams) -> str | None:
+        """None when applicable, else the reason (variants.py:206-210).  The C
+        library's b2c_conv_applies is the single source of truth."""
+        if node.kind != self.kind:
+            return f"kind {node.kind} != {self.kind}"
+        if node.fused_activation not in (None, "relu"):
+            return f"no fused form for activation '{node.fused_activation}'"
+        return backend.applies(conv_desc(node, edges), self.tune_struct(params))
+
+    def required_formats(self, node: OpNode, edges, params: TuneParams) -> VariantFormats:
+        return VariantFormats()
+
+    def default_params(self, node: OpNode, edges) -> TuneParams:
+        return DEFAULT_TUNE
+
+    def space(self, node: OpNode, edges) -> list:
+        """This variant's own candidate list for the on-device sweep."""
+        return [self.default_params(node, edges)]
+
+    def tune_candidates(self, node: OpNode, edges, candidates):
+        return [p for p in candidates if self.applies(node, edges, p) is None]
+
+    def generate(self, node: OpNode, edges, params: TuneParams, mode: str = STATIC) -> KernelPlan:
+        reason = self.applies(node, edges, params)
+        if reason:
+            raise Inapplicable(f"{self.name} on '{node.name}': {reason}")
+        return KernelPlan(self.name, conv_desc(node, edges), self.tune_struct(params), params)
+
+
+class ConvSimple(Variant):
+    name, rank, vid = "conv_simple", 0, backend.VAR_SIMPLE
+
+
+class ConvTiled(Variant):
+    name, rank, vid = "conv_tiled", 1, backend.VAR_TILED
+
+    def space(self, node, edges):
+        out = []
+        for mnt in ((4, 4), (8, 8), (8, 4), (4, 8)):
+            for mnb in ((16, 16), (32, 8), (8, 32), (16, 8)):
+                for kb in (8, 16):
+                    out.append(TuneParams(mnt=mnt, mnb=mnb, kb=kb, vw=4))
+        return [p for p in out if self.applies(node, edges, p) is None]
+
+
+def _ceil(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+class _UmmaFamily(Variant):
+    """tcgen05 3xTF32 implicit GEMM; ``kmode`` is fixed per registered name."""
+
+    def default_params(self, node, edges):
+        s = conv_shape(node, edges)
+        kblocks = _ceil(s.k, 32)
+
+        def plan(swap, bn):
+            rows_m, rows_n = (s.oc, s.m) if swap else (s.m, s.oc)
+            tiles = _ceil(rows_m, 128) * _ceil(rows_n, bn)
+            waste = _ceil(rows_m, 128) * 128 * _ceil(rows_n, bn) * bn
+            return tiles, waste
+
+        best = None
+        for swap in (False, True):
+            for bn in UMMA_BN:
+                tiles, waste = plan(swap, bn)
+                key = (waste, -bn)
+                if best is None or key < best[0]:
+                    best = (key, swap, bn, tiles)
+        _, swap, bn, tiles = best
+        split = 1
+        while tiles * split * 2 <= NUM_SMS and kblocks // (split * 2) >= 4:
+            split *= 2
+        return TuneParams(bn=bn, split_k=split, swap_ab=swap)
+
+    def space(self, node, edges):
+        s = conv_shape(node, edges)
+        kblocks = _ceil(s.k, 32)
+        out = []
+        for swap in (False, True):
+            n_rows = s.m if swap else s.oc
+            for bn in UMMA_BN:
+                if bn > 2 * max(32, n_rows):
+                    continue
+                for split in (1, 2, 4, 8, 16, 32):
+                    if split > 1 and kblocks // split < 2:
+                        continue
+                    out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap))
+        return [p for p in out if self.applies(node, edges, p) is None]
+
+
+class ConvUmma(_UmmaFamily):
+    name, rank, vid = "conv_umma", 2, backend.VAR_UMMA
+
+
+class Conv1x1(_UmmaFamily):
+    name, rank, vid = "conv_1x1", 3, backend.VAR_1X1
+
+
+class ConvFC(_UmmaFamily):
+    name, rank, vid = "conv_fc", 4, backend.VAR_FC
+
+
+VARIANTS: dict = {v.name: v for v in (ConvSimple(), ConvTiled(), ConvUmma(), Conv1x1(), ConvFC())}
+
+
+def variants_for_kind(kind: str) -> list:
+    """Variants for an op kind, most specialized first (variants.py:835-837)."""
+    return sorted((v for v in VARIANTS.values() if v.kind == kind), key=lambda v: -v.rank)
+
+
+def select_variant(node: OpNode, edges, db=None):
+    """(variant, params) for one node: the TuneDB record for its signature if
+    present, else the most specialized applicable variant (variants.py:840-856)."""
+    if db is not None:
+        from .tuner import op_signature
+
+        rec = db.records.get(op_signature(node, edges))
+        if rec is not None:
+            return VARIANTS[rec.variant], rec.params
+    for v in variants_for_kind(node.kind):
+        params = v.default_params(node, edges)
+        if v.applies(node, edges, params) is None:
+            return v, params
+    raise Inapplicable(f"no variant for node '{node.name}' of kind {node.kind}")

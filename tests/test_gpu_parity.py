@@ -1,0 +1,201 @@
+"""GPU parity: every variant through the C ABI vs the CPU oracle (and the
+reference's own golden outputs), at the reference tolerance.
+
+fp32 mode tolerance (stated): the reference rule verbatim —
+|a-b| <= max(1e-6, rel*max(|a|,|b|)), rel = 1e-5 for ic*k*k <= 4096 else 1e-3
+(cuclgen/oracle.py:31-38, :124-137).  Signed-input suite: |a-b| <= 1e-5 *
+sum|x||w| + 1e-6, with ReLU required to clip exactly.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import conv_ref
+from tests import golden_cases
+
+pytestmark = pytest.mark.gpu
+
+CASES, ARRAYS = golden_cases.load()
+
+
+def _graph(case_or_op, relu):
+    from paper_1611_06945_b200.frontend import ConvParams, conv_graph, with_fused
+    from paper_1611_06945_b200.ndarray import DimsSpec
+
+    c = case_or_op
+    p = ConvParams(ksz=c["ksz"], stride=c["stride"], pad=c["pad"], out_chans=c["out_chans"])
+    g = conv_graph(p, DimsSpec.row_major(("img", "chan", "y", "x"), c["in"]))
+    return with_fused(g, "conv", "relu") if relu else g
+
+
+def _run_device(g, x, f, b, vname, params):
+    import torch
+
+    from paper_1611_06945_b200 import runner
+    from paper_1611_06945_b200.variants import VARIANTS
+
+    node = g.node("conv")
+    plan = VARIANTS[vname].generate(node, g.edges, params)
+    op = runner.ConvOp(plan, *(torch.from_numpy(a).cuda() for a in (x, f, b)))
+    op.y.fill_(float("nan"))
+    op.launch()
+    torch.cuda.synchronize()
+    return op.y.cpu().numpy()
+
+
+def _variant_params(g):
+    """(variant, params) pairs exercised on each case: every applicable variant,
+    tcgen05 in both orientations and with split-K."""
+    from paper_1611_06945_b200.variants import VARIANTS, TuneParams
+
+    node = g.node("conv")
+    out = [("conv_simple", TuneParams()), ("conv_tiled", TuneParams(mnt=(4, 4), mnb=(8, 8), kb=8, vw=4)),
+           ("conv_tiled", TuneParams(mnt=(2, 2), mnb=(4, 4), kb=3, vw=2))]
+    for v in ("conv_umma", "conv_1x1", "conv_fc"):
+        for prm in (TuneParams(bn=32), TuneParams(bn=128, swap_ab=True), TuneParams(bn=64, split_k=2)):
+            out.append((v, prm))
+    return [(n, p) for n, p in out if VARIANTS[n].applies(node, g.edges, p) is None]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["id"] for c in CASES])
+def test_golden_cases_all_variants(cuda, case):
+    g = _graph(case, case["act"] == "relu")
+    x, f, b = golden_cases.inputs(case)
+    want, step = golden_cases.expected(case, ARRAYS)
+    tol = conv_ref.tolerance_for(case["reduction_terms"])
+    checked = 0
+    for vname, params in _variant_params(g):
+        got = _run_device(g, x, f, b, vname, params)
+        assert list(got.shape) == case["out_shape"]
+        res = conv_ref.compare(got.reshape(-1)[::step], want, tol)
+        assert res.ok, (vname, params.to_string(), res)
+        checked += 1
+    assert checked >= 3
+
+
+def test_tiled_equals_simple_bit_exact(cuda):
+    """Same fmaf sequence per output => identical bits (tests/test_variants.py:173-179)."""
+    from paper_1611_06945_b200.variants import TuneParams
+
+    case = {"ksz": 3, "stride": 1, "pad": 1, "out_chans": 5, "in": [2, 3, 6, 6]}
+    g = _graph(case, False)
+    x, f, b = conv_ref.conv_inputs(2, 3, 6, 6, 5, 3, "deg")
+    s = _run_device(g, x, f, b, "conv_simple", TuneParams())
+    for prm in (TuneParams(mnt=(1, 1), mnb=(1, 1), kb=1, vw=1), TuneParams(mnt=(4, 4), mnb=(8, 8), kb=8, vw=4),
+                TuneParams(mnt=(8, 2), mnb=(4, 2), kb=5, vw=2)):
+        t = _run_device(g, x, f, b, "conv_tiled", prm)
+        assert np.array_equal(s, t), prm.to_string()
+
+
+def _corpus_cases(batches):
+    from paper_1611_06945_b200 import corpus
+
+    out = []
+    for bt in batches:
+        for i, op in enumerate(corpus.corpus()):
+            o = op.with_batch(bt)
+            out.append(pytest.param(i, o, id=f"row{i:02d}-N{bt}"))
+    return out
+
+
+@pytest.mark.parametrize("row,op", _corpus_cases((1, 5, 20)))
+def test_corpus_heuristic_variant_vs_oracle(cuda, row, op):
+    """Every conv of the AlexNet/NiN/GoogLeNet sweep at N=1/5/20 with fused ReLU,
+    on the variant select_variant picks (the shipped TuneDB when present)."""
+    from paper_1611_06945_b200 import tuner
+    from paper_1611_06945_b200.frontend import with_fused
+    from paper_1611_06945_b200.variants import select_variant
+    import os
+
+    g = with_fused(op.graph(), "conv", "relu")
+    node = g.node("conv")
+    db = tuner.load_db(tuner.shipped_db_path()) if os.path.exists(tuner.shipped_db_path()) else None
+    v, params = select_variant(node, g.edges, db)
+    x, f, b = conv_ref.conv_inputs(op.batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz,
+                                   f"bench:{tuner.op_signature(node, g.edges)}")
+    got = _run_device(g, x, f, b, v.name, params)
+    want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
+    res = conv_ref.compare(got, want, conv_ref.tolerance_for(op.in_chans * op.ksz ** 2))
+    assert res.ok, (row, v.name, params.to_string(), res)
+
+
+@pytest.mark.parametrize("vname", ["conv_simple", "conv_tiled", "conv_umma"])
+def test_signed_inputs_relu_clips(cuda, vname):
+    from paper_1611_06945_b200.variants import TuneParams
+
+    case = {"ksz": 3, "stride": 1, "pad": 1, "out_chans": 48, "in": [2, 40, 14, 14]}
+    g = _graph(case, True)
+    x, f, b = conv_ref.conv_inputs(2, 40, 14, 14, 48, 3, "signed", low=-1.0, high=1.0)
+    params = {"conv_simple": TuneParams(), "conv_tiled": TuneParams(mnt=(4, 4), mnb=(8, 8), kb=8, vw=4),
+              "conv_umma": TuneParams(bn=64)}[vname]
+    got = _run_device(g, x, f, b, vname, params)
+    plain = conv_ref.ref_conv(x, f, b, 1, 1)
+    want = np.maximum(plain, 0)
+    bound = 1e-5 * conv_ref.signed_bound(x, f, 1, 1) + 1e-6
+    assert np.all(np.abs(got.astype(np.float64) - want) <= bound)
+    clipped = plain < -bound
+    assert clipped.any() and np.all(got[clipped] == 0.0)
+
+
+def test_split_k_deterministic(cuda):
+    from paper_1611_06945_b200.variants import TuneParams
+
+    case = {"ksz": 3, "stride": 1, "pad": 1, "out_chans": 256, "in": [1, 384, 13, 13]}
+    g = _graph(case, True)
+    x, f, b = conv_ref.conv_inputs(1, 384, 13, 13, 256, 3, "splitk")
+    runs = [_run_device(g, x, f, b, "conv_umma", TuneParams(bn=128, split_k=8)) for _ in range(3)]
+    assert all(np.array_equal(runs[0], r) for r in runs[1:])
+    want = conv_ref.ref_conv(x, f, b, 1, 1, relu=True)
+    assert conv_ref.compare(runs[0], want, conv_ref.tolerance_for(384 * 9)).ok
+
+
+def test_execute_node_and_host_e2e(cuda):
+    """The public API: execute_node (host NdArrays in/out) and the C-ABI host call."""
+    from paper_1611_06945_b200 import runner
+    from paper_1611_06945_b200.variants import VARIANTS, TuneParams
+
+    case = {"ksz": 5, "stride": 1, "pad": 2, "out_chans": 32, "in": [3, 16, 28, 28]}
+    g = _graph(case, True)
+    node = g.node("conv")
+    inputs = runner.node_test_inputs(node, g.edges, "e2e")
+    x, f, b = (inputs[e].to_np() for e in node.inputs)
+    want = conv_ref.ref_conv(x, f, b, 1, 2, relu=True)
+    got, rep = runner.execute_node(node, g.edges, inputs, VARIANTS["conv_umma"], TuneParams(bn=32))
+    assert got.dims.names == ("img", "chan", "y", "x") and rep.wall_ns > 0
+    assert conv_ref.compare(got.to_np(), want, conv_ref.tolerance_for(400)).ok
+    plan = VARIANTS["conv_umma"].generate(node, g.edges, TuneParams(bn=32, split_k=2))
+    hr = runner.HostRun.create(plan, x, f, b)
+    hr.run()
+    cuda.cuda.synchronize()
+    assert np.array_equal(hr.hy.numpy(), got.to_np()) or conv_ref.compare(hr.hy.numpy(), want, conv_ref.tolerance_for(400)).ok
+
+
+def test_sweep_on_device_and_db_roundtrip(cuda, tmp_path):
+    from paper_1611_06945_b200 import tuner
+    from paper_1611_06945_b200.variants import VARIANTS, select_variant
+
+    case = {"ksz": 3, "stride": 1, "pad": 1, "out_chans": 64, "in": [1, 32, 14, 14]}
+    g = _graph(case, True)
+    node = g.node("conv")
+    rec = tuner.sweep(node, g.edges, reps=3, warmup=1)
+    assert rec.variant in VARIANTS and rec.objective == "wall" and rec.cost > 0
+    db = tuner.TuneDB()
+    db.add(rec)
+    tuner.save_db(db, tmp_path / "db.tsv")
+    db2 = tuner.load_db(tmp_path / "db.tsv")
+    assert db2 == db
+    v, params = select_variant(node, g.edges, db2)
+    assert v.name == rec.variant and params == rec.params
+
+
+def test_bad_args_raise(cuda):
+    import torch
+
+    from paper_1611_06945_b200 import backend
+    from paper_1611_06945_b200.errors import ShapeMismatch
+
+    d = backend.make_desc(1, 3, 8, 8, 4, 3, 1, 1, 7, 8, False)  # wrong oh
+    t = backend.Tune(backend.VAR_SIMPLE, 1, 1, 1, 1, 1, 1, 32, 0, 1, 0)
+    z = torch.zeros(1024, device="cuda")
+    with pytest.raises(ShapeMismatch):
+        backend.fwd(d, t, z, z, z, z)
