@@ -81,19 +81,35 @@ typedef struct b2c_conv_desc {
 /* Variant + tuning knobs, the C form of TuneParams (variants.py:39-91).
  * FFMA variants read mnt/mnb/kb/vw with the reference's meaning (register
  * block, thread block, k unroll, vector width).  The tcgen05 variants read
- * tile_n (MMA N), stages, split_k and swap_ab (0: M = output pixels, N =
- * out_chans; 1: M = out_chans, N = output pixels). */
+ * tile_n (MMA N), stages (< 0 disables the cooperative L2 prefetch of x/w
+ * that small ops get by default), split_k, swap_ab (0: M = output pixels, N =
+ * out_chans; 1: M = out_chans, N = output pixels) and drain (K blocks of 32
+ * accumulated in one TMEM chunk before it is drained into fp32 registers;
+ * 0 = default 4 — bounds the tensor-core accumulation error, see k_umma.cuh).
+ * prepared != 0 asserts the workspace already holds this filter tensor packed
+ * by b2c_conv_prepare (filters are constant per op; the pack is cached per
+ * (filter tensor, variant) as SURVEY.md §8(b) specifies); prepared == 0 makes
+ * b2c_conv_fwd pack the filters itself first (one extra launch). */
 typedef struct b2c_tune {
     int32_t variant;
     int32_t mnt0, mnt1, mnb0, mnb1, kb, vw;
-    int32_t tile_n, stages, split_k, swap_ab;
+    int32_t tile_n, stages, split_k, swap_ab, drain, prepared;
 } b2c_tune;
 
 /* 0 when `tune` can run `d`; otherwise B2C_INAPPLICABLE / B2C_BAD_ARGS with a
  * reason copied into reason[0..n) (Variant.applies, variants.py:206-210). */
 int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, size_t n);
 
-/* Device workspace bytes b2c_conv_fwd needs (split-K partials + semaphores).
+/* Pack the filters w (OIHW fp32) into the workspace in the layout the tcgen05
+ * variants stream with cp.async.bulk: per (filter tile, K block) the exact
+ * shared-memory image [raw | lo = w - trunc_tf32(w)].  No-op (B2C_OK) for the
+ * FFMA variants.  This is the B200 form of ConvTiled.required_formats
+ * (variants.py:416-424: K-major padded filters) + the conversion execute_node
+ * applies (runner.py:96-98), done once per filter tensor instead of per call. */
+int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* workspace,
+                     size_t ws_bytes, void* stream);
+
+/* Device workspace bytes b2c_conv_fwd needs (packed filters + split-K partials + semaphores).
  * The workspace must be zero-filled once before first use (semaphores reset
  * themselves after every launch). */
 size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t);

@@ -30,6 +30,7 @@ PREC_FP32, PREC_BF16 = 0, 1
 # Every symbol include/b2conv.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "b2c_conv_applies",
+    "b2c_conv_prepare",
     "b2c_conv_workspace",
     "b2c_conv_fwd",
     "b2c_conv_time",
@@ -49,7 +50,7 @@ class ConvDesc(ctypes.Structure):
 
 class Tune(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
-        "variant", "mnt0", "mnt1", "mnb0", "mnb1", "kb", "vw", "tile_n", "stages", "split_k", "swap_ab")]
+        "variant", "mnt0", "mnt1", "mnb0", "mnb1", "kb", "vw", "tile_n", "stages", "split_k", "swap_ab", "drain", "prepared")]
 
 
 _lib = None
@@ -68,6 +69,7 @@ def lib():
         P = ctypes.POINTER
         vp, sz = ctypes.c_void_p, ctypes.c_size_t
         L.b2c_conv_applies.argtypes = [P(ConvDesc), P(Tune), ctypes.c_char_p, sz]
+        L.b2c_conv_prepare.argtypes = [P(ConvDesc), P(Tune), vp, vp, sz, vp]
         L.b2c_conv_workspace.argtypes = [P(ConvDesc), P(Tune)]
         L.b2c_conv_workspace.restype = sz
         L.b2c_conv_fwd.argtypes = [P(ConvDesc), P(Tune), vp, vp, vp, vp, vp, sz, vp]
@@ -145,6 +147,15 @@ def fwd(desc: ConvDesc, tune: Tune, x, w, bias, y, ws=None, stream=None):
     rc = lib().b2c_conv_fwd(ctypes.byref(desc), ctypes.byref(tune), x.data_ptr(), w.data_ptr(), bias.data_ptr(),
                             y.data_ptr(), ws_ptr, ws_len, st)
     check(rc, "b2c_conv_fwd")
+
+
+def prepare(desc: ConvDesc, tune: Tune, w, ws, stream=None):
+    """Pack the filters into the workspace (b2c_conv_prepare). Async."""
+    torch = _require_cuda()
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    ws_ptr, ws_len = (ws.data_ptr(), ws.numel() * ws.element_size()) if ws is not None else (None, 0)
+    check(lib().b2c_conv_prepare(ctypes.byref(desc), ctypes.byref(tune), w.data_ptr(), ws_ptr, ws_len, st),
+          "b2c_conv_prepare")
 
 
 def time_ms(desc: ConvDesc, tune: Tune, x, w, bias, y, ws=None, warmup=3, reps=10, l2_flush=True, stream=None) -> float:

@@ -77,7 +77,20 @@ Geom make_geom(const b2c_conv_desc* d) {
     return g;
 }
 
-bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || bn == 192 || bn == 256; }
+bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || bn == 192; }
+
+// K order of the tcgen05 kernels: tap-major (3) when there are >= 32 input
+// channels, flat (0) for first layers, flat contiguous (2) for conv_fc.
+int kmode_for(const b2c_conv_desc* d, int variant) {
+    if (variant == B2C_VAR_FC) return 2;
+    if (variant == B2C_VAR_1X1) return 3;
+    return d->c >= 32 ? 3 : 0;
+}
+
+int kblocks_for(const b2c_conv_desc* d, int kmode) {
+    if (kmode == 3) return d->r * d->r * ((d->c + 31) / 32);
+    return (d->c * d->r * d->r + 31) / 32;
+}
 
 int is_pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; }
 
@@ -124,11 +137,11 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             return B2C_BAD_ARGS;
     }
     // tcgen05 family
-    if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192,256"; return B2C_INAPPLICABLE; }
+    if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192"; return B2C_INAPPLICABLE; }
     if (t->split_k < 1) { why = "split_k must be >= 1"; return B2C_BAD_ARGS; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
-    const int K = d->c * d->r * d->r;
-    const int kblocks = (K + UMMA_BK - 1) / UMMA_BK;
+    if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
+    const int kblocks = kblocks_for(d, kmode_for(d, t->variant));
     if (t->split_k > kblocks) { why = "split_k exceeds the number of 32-wide K blocks"; return B2C_INAPPLICABLE; }
     return B2C_OK;
 }
@@ -136,46 +149,49 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
 // ----------------------------------------------------------------------------- launch plans
 
 struct UmmaPlan {
-    int grid_x, grid_y, split, kps, kblocks, tiles;
-    size_t ws_bytes;  // partials + semaphores
+    int grid_x, grid_y, split, kps, kblocks, cblocks, tiles, kmode, flt_rows;
+    size_t wpk_bytes;   // packed filters (offset 0 of the workspace)
+    size_t part_off;    // split-K partials
+    size_t sems_off;    // split-K tickets
+    size_t ws_bytes;    // total
 };
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     UmmaPlan p;
-    const int K = d->c * d->r * d->r;
     const int M = d->n * d->oh * d->ow;
     const int BN = t->tile_n;
     const int pix_tile = t->swap_ab ? BN : UMMA_M;
-    const int oc_tile = t->swap_ab ? UMMA_M : BN;
+    p.flt_rows = t->swap_ab ? UMMA_M : BN;
     p.grid_x = (M + pix_tile - 1) / pix_tile;
-    p.grid_y = (d->k + oc_tile - 1) / oc_tile;
+    p.grid_y = (d->k + p.flt_rows - 1) / p.flt_rows;
     p.tiles = p.grid_x * p.grid_y;
-    p.kblocks = (K + UMMA_BK - 1) / UMMA_BK;
+    p.kmode = kmode_for(d, t->variant);
+    p.kblocks = kblocks_for(d, p.kmode);
+    p.cblocks = (d->c + 31) / 32;
     const int want = std::max(1, std::min(t->split_k, p.kblocks));
     p.kps = (p.kblocks + want - 1) / want;
     p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
-    p.ws_bytes = 0;
-    if (p.split > 1) {
-        p.ws_bytes = (size_t)p.tiles * p.split * BN * UMMA_M * sizeof(float);
-        p.ws_bytes = (p.ws_bytes + 255) & ~(size_t)255;
-        p.ws_bytes += (size_t)p.tiles * sizeof(int);
-    }
+    p.wpk_bytes = (size_t)p.grid_y * p.kblocks * 2 * p.flt_rows * UMMA_BK * sizeof(float);
+    p.part_off = align256(p.wpk_bytes);
+    p.sems_off = p.part_off;
+    if (p.split > 1) p.sems_off += align256((size_t)p.tiles * p.split * BN * UMMA_M * sizeof(float));
+    p.ws_bytes = p.sems_off + (p.split > 1 ? align256((size_t)p.tiles * sizeof(int)) : 0);
     return p;
 }
 
 using UmmaKernel = void (*)(UmmaArgs);
 
-template <int BN, bool SWAP, int KMODE>
-int umma_smem() { return UmmaCfg<BN>::SMEM; }
-
 struct UmmaEntry {
     UmmaKernel fn;
     int smem;
+    int stages;
 };
 
 template <int BN, bool SWAP, int KMODE>
 UmmaEntry umma_entry() {
-    return UmmaEntry{&k_umma<BN, SWAP, KMODE>, UmmaCfg<BN>::SMEM};
+    return UmmaEntry{&k_umma<BN, SWAP, KMODE>, UmmaCfg<BN, SWAP>::SMEM, UmmaCfg<BN, SWAP>::STAGES};
 }
 
 template <bool SWAP, int KMODE>
@@ -186,23 +202,34 @@ UmmaEntry umma_pick_bn(int bn) {
         case 96: return umma_entry<96, SWAP, KMODE>();
         case 128: return umma_entry<128, SWAP, KMODE>();
         case 192: return umma_entry<192, SWAP, KMODE>();
-        case 256: return umma_entry<256, SWAP, KMODE>();
     }
-    return UmmaEntry{nullptr, 0};
+    return UmmaEntry{nullptr, 0, 0};
 }
 
 UmmaEntry umma_pick(int bn, int swap, int kmode) {
     if (swap) {
         if (kmode == 0) return umma_pick_bn<true, 0>(bn);
-        if (kmode == 1) return umma_pick_bn<true, 1>(bn);
-        return umma_pick_bn<true, 2>(bn);
+        if (kmode == 2) return umma_pick_bn<true, 2>(bn);
+        return umma_pick_bn<true, 3>(bn);
     }
     if (kmode == 0) return umma_pick_bn<false, 0>(bn);
-    if (kmode == 1) return umma_pick_bn<false, 1>(bn);
-    return umma_pick_bn<false, 2>(bn);
+    if (kmode == 2) return umma_pick_bn<false, 2>(bn);
+    return umma_pick_bn<false, 3>(bn);
 }
 
-int kmode_of(int variant) { return variant == B2C_VAR_1X1 ? 1 : variant == B2C_VAR_FC ? 2 : 0; }
+bool is_umma(int variant) { return variant == B2C_VAR_UMMA || variant == B2C_VAR_1X1 || variant == B2C_VAR_FC; }
+
+int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+    const UmmaPlan p = umma_plan(d, t);
+    if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+    const Geom g = make_geom(d);
+    const long long total = (long long)p.wpk_bytes / 4;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+    k_pack_filters<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<float*>(ws), p.flt_rows, p.kblocks,
+                                           FastDiv((uint32_t)p.cblocks), p.kmode, total);
+    return B2C_OK;
+}
 
 // Per-device "max dynamic smem" attribute is set once per kernel.
 std::mutex g_attr_mu;
@@ -259,22 +286,34 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
         }
         default: {
             const UmmaPlan p = umma_plan(d, t);
-            UmmaEntry e = umma_pick(t->tile_n, t->swap_ab, kmode_of(t->variant));
+            UmmaEntry e = umma_pick(t->tile_n, t->swap_ab, p.kmode);
             if (!e.fn) return fail(B2C_INAPPLICABLE, "no tcgen05 kernel for this tile");
-            if (p.split > 1 && (!ws || ws_bytes < p.ws_bytes))
-                return fail(B2C_BAD_ARGS, "workspace too small for split-K (see b2c_conv_workspace)");
+            if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+            if (!t->prepared) {
+                rc = pack_impl(d, t, w, ws, ws_bytes, st);
+                if (rc) return rc;
+            }
             rc = ensure_smem_attr((const void*)e.fn, e.smem);
             if (rc) return rc;
             UmmaArgs a;
             a.g = g;
-            a.x = x; a.w = w; a.bias = bias; a.y = y;
-            a.split = p.split; a.kps = p.kps; a.kblocks = p.kblocks;
-            a.ws = reinterpret_cast<float*>(ws);
-            a.sems = nullptr;
-            if (p.split > 1) {
-                const size_t part = ((size_t)p.tiles * p.split * t->tile_n * UMMA_M * sizeof(float) + 255) & ~(size_t)255;
-                a.sems = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + part);
+            a.x = x;
+            a.wpk = reinterpret_cast<const float*>(ws);
+            a.bias = bias;
+            a.y = y;
+            a.split = p.split;
+            a.kps = p.kps;
+            a.kblocks = p.kblocks;
+            a.fCB = FastDiv((uint32_t)p.cblocks);
+            a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
+            a.lag = std::max(0, std::min(a.drain - 2, e.stages - 1));
+            a.wpk_elems = (long long)p.wpk_bytes / 4;
+            {
+                const long long op_bytes = 4ll * ((long long)d->n * d->c * d->h * d->w) + (long long)p.wpk_bytes;
+                a.prefetch = (t->stages >= 0 && op_bytes <= (48ll << 20)) ? 1 : 0;  // stages < 0: disable
             }
+            a.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + p.part_off);
+            a.sems = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + p.sems_off);
             dim3 grid(p.grid_x, p.grid_y, p.split);
             e.fn<<<grid, UMMA_THREADS, e.smem, st>>>(a);
             break;
@@ -326,8 +365,22 @@ int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, si
 size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t) {
     std::string why;
     if (applies_impl(d, t, why)) return 0;
-    if (t->variant == B2C_VAR_SIMPLE || t->variant == B2C_VAR_TILED) return 0;
+    if (!is_umma(t->variant)) return 0;
     return umma_plan(d, t).ws_bytes;
+}
+
+int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* workspace, size_t ws_bytes,
+                     void* stream) {
+    std::string why;
+    int rc = applies_impl(d, t, why);
+    if (rc) return fail(rc, why);
+    if (!is_umma(t->variant)) return B2C_OK;
+    if (!w) return fail(B2C_BAD_ARGS, "null filter pointer");
+    rc = pack_impl(d, t, w, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) return cuda_fail(le, "pack launch");
+    return B2C_OK;
 }
 
 int b2c_conv_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias,
@@ -401,7 +454,9 @@ int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx
     B2C_CUDA(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, st));
     B2C_CUDA(cudaMemcpyAsync(dw, hw, wb, cudaMemcpyHostToDevice, st));
     B2C_CUDA(cudaMemcpyAsync(db, hbias, bb, cudaMemcpyHostToDevice, st));
-    rc = fwd_impl(d, t, dx, dw, db, dy, ws, wsb, st);
+    b2c_tune tt = *t;
+    tt.prepared = 0;  // filters arrive fresh from the host: pack them in this call
+    rc = fwd_impl(d, &tt, dx, dw, db, dy, ws, wsb, st);
     if (rc) return rc;
     B2C_CUDA(cudaMemcpyAsync(hy, dy, yb, cudaMemcpyDeviceToHost, st));
     return B2C_OK;
@@ -420,8 +475,8 @@ int64_t b2c_conv_bytes(const b2c_conv_desc* d) {
 
 int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
     (void)d;
-    (void)t;
-    return 1;
+    if (!t) return 0;
+    return (is_umma(t->variant) && !t->prepared) ? 2 : 1;
 }
 
 const char* b2c_last_error(void) { return g_last_error.c_str(); }

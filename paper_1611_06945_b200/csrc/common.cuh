@@ -71,6 +71,19 @@ __device__ __forceinline__ void mbar_fence_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;" ::"r"(bytes), "r"(bar) : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine, no tensor map); completes as tx
+// bytes on the mbarrier.  16-byte aligned addresses, size multiple of 16.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst_smem),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -94,6 +107,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     long long t0 = clock64();
     while (!mbar_try_wait(bar, parity)) {
         if (clock64() - t0 > (1ll << 31)) __trap();
+    }
+}
+
+// Bulk L2 prefetch of [p, p+bytes): 16-byte aligned address, size multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// This CTA's 1/ncta share of a tensor, prefetched into L2 (whole-grid cooperative).
+__device__ __forceinline__ void prefetch_share_l2(const float* base, long long elems, int cta, int ncta) {
+    const long long bytes = elems * 4;
+    long long chunk = ((bytes + ncta - 1) / ncta + 4095) & ~4095ll;
+    const long long lo = (long long)cta * chunk;
+    if (lo >= bytes) return;
+    long long n = bytes - lo < chunk ? bytes - lo : chunk;
+    n &= ~15ll;
+    const char* p = reinterpret_cast<const char*>(base) + lo;
+    while (n > 0) {
+        const uint32_t step = n > (1ll << 20) ? (1u << 20) : (uint32_t)n;
+        prefetch_l2_bulk(p, step);
+        p += step;
+        n -= step;
     }
 }
 
@@ -162,6 +197,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 32 TMEM lanes x 8 consecutive 32-bit columns -> 8 registers per thread.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // UMMA shared-memory matrix descriptor, K-major, SWIZZLE_NONE ("interleaved"):

@@ -54,8 +54,11 @@ __global__ void __launch_bounds__(256) k_simple(Geom g, const float* __restrict_
 //   Bs   [KB][BN]  filter tile
 //   pix  [BM] int4 {x offset of (b, iy0, ix0), iy0, ix0, valid}
 //   ktab [KB] int4 {ic*HW + ky*W + kx, ky, kx, valid}
+__host__ __device__ inline int tiled_tab_offset(int BM, int BN, int KB) {  // in floats, 16-byte aligned
+    return (KB * (BM + BN) + 3) & ~3;
+}
 __host__ __device__ inline size_t tiled_smem_bytes(int BM, int BN, int KB) {
-    return (size_t)KB * (BM + BN) * 4 + (size_t)BM * 16 + (size_t)KB * 16;
+    return (size_t)tiled_tab_offset(BM, BN, KB) * 4 + (size_t)BM * 16 + (size_t)KB * 16;
 }
 
 template <int MT, int NT>
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(1024) k_tiled(Geom g, const float* __restrict_
     const int BM = MB * MT, BN = NB * NT;
     float* As = smf;
     float* Bs = smf + KB * BM;
-    int4* pix = reinterpret_cast<int4*>(smf + KB * (BM + BN));
+    int4* pix = reinterpret_cast<int4*>(smf + tiled_tab_offset(BM, BN, KB));
     int4* ktab = pix + BM;
 
     const int tid = threadIdx.x;

@@ -62,7 +62,13 @@ def _torch():
 
 
 class ConvOp:
-    """One conv bound to device operands and a kernel plan; ``launch()`` = one kernel."""
+    """One conv bound to device operands and a kernel plan; ``launch()`` = one kernel.
+
+    Filters are constant per op: at construction the tcgen05 variants pack them
+    once into the workspace (b2c_conv_prepare — the cached filter transform of
+    SURVEY.md §8(b); the reference's ConvTiled asks for re-laid-out filters via
+    required_formats, variants.py:416-424).  ``prepare()`` re-packs after the
+    filter tensor changes."""
 
     def __init__(self, plan: KernelPlan, x, w, bias, y=None, device=None):
         torch = _torch()
@@ -75,6 +81,14 @@ class ConvOp:
         self.x, self.w, self.bias = x, w, bias
         self.y = y if y is not None else torch.empty((d.n, d.k, d.oh, d.ow), dtype=torch.float32, device=dev)
         self.ws = backend.alloc_workspace(d, plan.tune, device=dev)
+        self.tune = backend.Tune.from_buffer_copy(plan.tune)
+        self.prepare()
+
+    def prepare(self, stream=None):
+        """Pack the filters (tcgen05 variants) and mark the plan prepared."""
+        self.tune.prepared = 0
+        backend.prepare(self.plan.desc, self.tune, self.w, self.ws, stream)
+        self.tune.prepared = 1
 
     @property
     def flops(self) -> int:
@@ -85,11 +99,23 @@ class ConvOp:
         return backend.conv_bytes(self.plan.desc)
 
     def launch(self, stream=None):
-        backend.fwd(self.plan.desc, self.plan.tune, self.x, self.w, self.bias, self.y, self.ws, stream)
+        backend.fwd(self.plan.desc, self.tune, self.x, self.w, self.bias, self.y, self.ws, stream)
 
     def time_ms(self, warmup=3, reps=10, l2_flush=True) -> float:
-        return backend.time_ms(self.plan.desc, self.plan.tune, self.x, self.w, self.bias, self.y, self.ws,
+        return backend.time_ms(self.plan.desc, self.tune, self.x, self.w, self.bias, self.y, self.ws,
                                warmup, reps, l2_flush)
+
+    def prepare_ms(self) -> float:
+        """Device time of one filter pack (0 for variants that need none)."""
+        torch = _torch()
+        if self.ws is None:
+            return 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self.prepare()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1)
 
 
 def to_device(nda: NdArray, device="cuda"):

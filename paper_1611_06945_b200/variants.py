@@ -33,7 +33,7 @@ from .frontend import KIND_CONV, OpNode
 STATIC = "static"
 DYNAMIC = "dynamic"
 
-UMMA_BN = (32, 64, 96, 128, 192, 256)
+UMMA_BN = (32, 64, 96, 128, 192)
 NUM_SMS = 148
 
 
@@ -52,6 +52,7 @@ class TuneParams:
     bn: int = 128
     split_k: int = 1
     swap_ab: bool = False
+    drain: int = 0  # K blocks per TMEM chunk before the fp32 register drain (0 = library default)
 
     def __post_init__(self):
         if min(self.mnt) < 1 or min(self.mnb) < 1 or self.kb < 1:
@@ -62,7 +63,7 @@ class TuneParams:
             raise CuclgenError(f"vector width must be one of 1,2,4,8, got {self.vw}")
         if self.mnt[1] % self.vw:
             raise CuclgenError(f"vector width {self.vw} must divide register block {self.mnt[1]}")
-        if self.bn < 1 or self.split_k < 1:
+        if self.bn < 1 or self.split_k < 1 or self.drain < 0:
             raise CuclgenError(f"bad tcgen05 tile params {self}")
 
     @property
@@ -72,7 +73,7 @@ class TuneParams:
     def to_string(self) -> str:
         return (f"MNt={self.mnt[0]}:{self.mnt[1]},MNb={self.mnb[0]}:{self.mnb[1]},Kb={self.kb},vw={self.vw},"
                 f"lf={int(self.use_local_filts)},li={int(self.use_local_in)},"
-                f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)}")
+                f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)},dr={self.drain}")
 
     @staticmethod
     def from_string(text: str) -> "TuneParams":
@@ -89,6 +90,7 @@ class TuneParams:
                 bn=int(kv.get("BN", "128")),
                 split_k=int(kv.get("sk", "1")),
                 swap_ab=kv.get("sw", "0") == "1",
+                drain=int(kv.get("dr", "0")),
             )
         except (KeyError, ValueError) as e:
             raise CuclgenError(f"bad tune-params string {text!r}: {e}") from None
@@ -167,7 +169,7 @@ class Variant:
 
     def tune_struct(self, params: TuneParams) -> backend.Tune:
         return backend.Tune(self.vid, params.mnt[0], params.mnt[1], params.mnb[0], params.mnb[1], params.kb,
-                            params.vw, params.bn, 0, params.split_k, int(params.swap_ab))
+                            params.vw, params.bn, 0, params.split_k, int(params.swap_ab), params.drain, 0)
 
     def applies(self, node: OpNode, edges, params: TuneParams) -> str | None:
         """None when applicable, else the reason (variants.py:206-210).  The C

@@ -50,7 +50,7 @@ def _desc(**kw):
 
 
 def _tune(variant, **kw):
-    t = dict(mnt0=4, mnt1=4, mnb0=16, mnb1=16, kb=4, vw=4, tile_n=128, stages=0, split_k=1, swap_ab=0)
+    t = dict(mnt0=4, mnt1=4, mnb0=16, mnb1=16, kb=4, vw=4, tile_n=128, stages=0, split_k=1, swap_ab=0, drain=0, prepared=0)
     t.update(kw)
     return backend.Tune(variant, *t.values())
 
@@ -68,6 +68,14 @@ def test_applicability_reasons():
     assert backend.applies(fc, _tune(backend.VAR_FC, tile_n=32, swap_ab=1, split_k=8)) is None
 
 
+def test_launch_counts():
+    d = _desc()
+    lib = backend.lib()
+    assert lib.b2c_conv_launches(ctypes.byref(d), ctypes.byref(_tune(backend.VAR_UMMA, tile_n=96))) == 2
+    assert lib.b2c_conv_launches(ctypes.byref(d), ctypes.byref(_tune(backend.VAR_UMMA, tile_n=96, prepared=1))) == 1
+    assert lib.b2c_conv_launches(ctypes.byref(d), ctypes.byref(_tune(backend.VAR_SIMPLE))) == 1
+
+
 def test_bad_descriptor_is_rejected():
     assert "inconsistent" in backend.applies(_desc(oh=54), _tune(backend.VAR_SIMPLE))
     assert backend.applies(_desc(stride=0), _tune(backend.VAR_SIMPLE))
@@ -75,10 +83,13 @@ def test_bad_descriptor_is_rejected():
 
 def test_workspace_and_work_accounting():
     d = _desc()
-    assert backend.workspace_bytes(d, _tune(backend.VAR_UMMA, tile_n=96)) == 0
+    kblocks = -(-363 // 32)  # C = 3 < 32: flat K order
+    packed = 1 * kblocks * 2 * 96 * 32 * 4  # one 96-row filter tile, raw + lo
+    assert backend.workspace_bytes(d, _tune(backend.VAR_SIMPLE)) == 0
+    assert backend.workspace_bytes(d, _tune(backend.VAR_UMMA, tile_n=96)) >= packed
     ws = backend.workspace_bytes(d, _tune(backend.VAR_UMMA, tile_n=96, split_k=4))
     tiles = -(-3025 // 128)
-    assert ws >= tiles * 4 * 96 * 128 * 4 + tiles * 4
+    assert ws >= packed + tiles * 4 * 96 * 128 * 4 + tiles * 4
     assert backend.conv_flops(d) == 210_830_400
     assert backend.conv_bytes(d) == 1_919_724
 

@@ -1,0 +1,52 @@
+#!/usr/bin/env python
+"""Autotune every op of the conv sweep on the local B200 and write a TuneDB.
+
+This is the B200 form of ``cuclgen tune`` (cli.py:125-140): one on-device
+sweep per distinct op signature (tuner.tune_all), objective ``wall``.  The
+result is shipped as paper_1611_06945_b200/data/tunedb_b200_fp32.tsv and read
+by select_variant / bench.py.
+
+    python tools/tune_sweep.py --out gpurun_out/tunedb_b200_fp32.tsv [--batches 1,5,20] [--reps 5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1611_06945_b200 import corpus, tuner  # noqa: E402
+from paper_1611_06945_b200.frontend import with_fused  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--batches", default="1,5,20")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--rows", default=None, help="comma list of corpus rows (default all)")
+    ap.add_argument("--merge", default=None, help="existing DB to merge into")
+    args = ap.parse_args()
+    db = tuner.load_db(args.merge) if args.merge and os.path.exists(args.merge) else tuner.TuneDB()
+    rows = None if args.rows is None else {int(r) for r in args.rows.split(",")}
+    t_all = time.time()
+    for row, op in corpus.sweep_ops([int(b) for b in args.batches.split(",")]):
+        if rows is not None and row not in rows:
+            continue
+        g = with_fused(op.graph(), "conv", "relu")
+        node = g.node("conv")
+        t0 = time.time()
+        rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2)
+        db.add(rec)
+        print(f"row{row:02d} N={op.batch:2d} {rec.op_signature:42s} {rec.variant:11s} {rec.params.to_string():60s} "
+              f"{rec.cost / 1e3:9.2f} us  {op.flops_computed / rec.cost / 1e3:7.1f} TFLOP/s  err={rec.max_rel_err:.2e}  "
+              f"({time.time() - t0:.1f}s)", flush=True)
+        tuner.save_db(db, args.out)
+    print(f"tuned {len(db.records)} signatures in {time.time() - t_all:.0f}s -> {args.out}")
+
+
+if __name__ == "__main__":
+    main()
