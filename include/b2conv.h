@@ -94,6 +94,9 @@ typedef struct b2c_tune {
     int32_t variant;
     int32_t mnt0, mnt1, mnb0, mnb1, kb, vw;
     int32_t tile_n, stages, split_k, swap_ab, drain, prepared;
+    int32_t tma; /* tcgen05 variants: 0 = operands gathered by producer warps from NCHW (k_umma);
+                    1 = TMA-fed (k_tconv): im2col TMA on an NHWC copy of x made in the workspace
+                    by the same call, or 2-D TMA of raw x / w for conv_fc */
 } b2c_tune;
 
 /* 0 when `tune` can run `d`; otherwise B2C_INAPPLICABLE / B2C_BAD_ARGS with a
@@ -109,7 +112,8 @@ int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, si
 int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* workspace,
                      size_t ws_bytes, void* stream);
 
-/* Device workspace bytes b2c_conv_fwd needs (packed filters + split-K partials + semaphores).
+/* Device workspace bytes b2c_conv_fwd needs (packed filters + split-K partials + semaphores
+ * + the NHWC copy of x for the TMA conv path).
  * The workspace must be zero-filled once before first use (semaphores reset
  * themselves after every launch). */
 size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t);

@@ -3,6 +3,7 @@
 // See include/b2conv.h for the contract and the reference call it replaces
 // (cuclgen/backend.py:1104-1133 run_kernel, via runner.execute_node
 // runner.py:73-106).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,8 +17,10 @@
 #include "common.cuh"
 #include "k_ffma.cuh"
 #include "k_umma.cuh"
+#include "k_tma.cuh"
 
 using namespace b2c;
+
 
 namespace {
 
@@ -81,9 +84,9 @@ bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || 
 
 // K order of the tcgen05 kernels: tap-major (3) when there are >= 32 input
 // channels, flat (0) for first layers, flat contiguous (2) for conv_fc.
-int kmode_for(const b2c_conv_desc* d, int variant) {
+int kmode_for(const b2c_conv_desc* d, int variant, int tma) {
     if (variant == B2C_VAR_FC) return 2;
-    if (variant == B2C_VAR_1X1) return 3;
+    if (variant == B2C_VAR_1X1 || tma) return 3;
     return d->c >= 32 ? 3 : 0;
 }
 
@@ -141,7 +144,19 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->split_k < 1) { why = "split_k must be >= 1"; return B2C_BAD_ARGS; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
-    const int kblocks = kblocks_for(d, kmode_for(d, t->variant));
+    if (t->tma < 0 || t->tma > 2) { why = "tma must be 0, 1 or 2"; return B2C_BAD_ARGS; }
+    if (t->tma == 2 && !(d->r == 1 && d->stride == 1 && d->pad == 0) && t->variant != B2C_VAR_FC) {
+        why = "tma=2 (2-D tiled pixels) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
+    }
+    if (t->tma) {
+        if (t->variant == B2C_VAR_FC) {
+            if ((d->c * d->r * d->r) % 4) { why = "TMA fc path needs ic*h*w % 4 == 0 (16-byte rows)"; return B2C_INAPPLICABLE; }
+        } else {
+            if (d->c % 4) { why = "TMA conv path needs in_chans % 4 == 0 (16-byte NHWC pixels)"; return B2C_INAPPLICABLE; }
+            if (d->pad > 127 || d->r - 1 - d->pad > 128 || d->r > 256) { why = "filter too large for TMA im2col"; return B2C_INAPPLICABLE; }
+        }
+    }
+    const int kblocks = kblocks_for(d, kmode_for(d, t->variant, t->tma));
     if (t->split_k > kblocks) { why = "split_k exceeds the number of 32-wide K blocks"; return B2C_INAPPLICABLE; }
     return B2C_OK;
 }
@@ -149,10 +164,11 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
 // ----------------------------------------------------------------------------- launch plans
 
 struct UmmaPlan {
-    int grid_x, grid_y, split, kps, kblocks, cblocks, tiles, kmode, flt_rows;
-    size_t wpk_bytes;   // packed filters (offset 0 of the workspace)
+    int grid_x, grid_y, split, kps, kblocks, cblocks, tiles, kmode, flt_rows, tma;
+    size_t wpk_bytes;   // packed filters (offset 0 of the workspace; 0 for the TMA fc path)
     size_t part_off;    // split-K partials
     size_t sems_off;    // split-K tickets
+    size_t nhwc_off;    // TMA conv path: NHWC copy of x
     size_t ws_bytes;    // total
 };
 
@@ -167,17 +183,20 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.grid_x = (M + pix_tile - 1) / pix_tile;
     p.grid_y = (d->k + p.flt_rows - 1) / p.flt_rows;
     p.tiles = p.grid_x * p.grid_y;
-    p.kmode = kmode_for(d, t->variant);
+    p.tma = t->tma;
+    p.kmode = kmode_for(d, t->variant, t->tma);
     p.kblocks = kblocks_for(d, p.kmode);
     p.cblocks = (d->c + 31) / 32;
     const int want = std::max(1, std::min(t->split_k, p.kblocks));
     p.kps = (p.kblocks + want - 1) / want;
     p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
-    p.wpk_bytes = (size_t)p.grid_y * p.kblocks * 2 * p.flt_rows * UMMA_BK * sizeof(float);
+    p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * 2 * p.flt_rows * UMMA_BK * sizeof(float);
     p.part_off = align256(p.wpk_bytes);
     p.sems_off = p.part_off;
     if (p.split > 1) p.sems_off += align256((size_t)p.tiles * p.split * BN * UMMA_M * sizeof(float));
-    p.ws_bytes = p.sems_off + (p.split > 1 ? align256((size_t)p.tiles * sizeof(int)) : 0);
+    p.nhwc_off = p.sems_off + (p.split > 1 ? align256((size_t)p.tiles * sizeof(int)) : 0);
+    const bool nhwc = p.tma && p.kmode == 3;
+    p.ws_bytes = p.nhwc_off + (nhwc ? align256((size_t)d->n * d->c * d->h * d->w * sizeof(float)) : 0);
     return p;
 }
 
@@ -222,12 +241,13 @@ bool is_umma(int variant) { return variant == B2C_VAR_UMMA || variant == B2C_VAR
 int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* ws, size_t ws_bytes,
               cudaStream_t st) {
     const UmmaPlan p = umma_plan(d, t);
+    if (p.wpk_bytes == 0) return B2C_OK;  // TMA fc path reads raw filters
     if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
     const Geom g = make_geom(d);
     const long long total = (long long)p.wpk_bytes / 4;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
     k_pack_filters<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<float*>(ws), p.flt_rows, p.kblocks,
-                                           FastDiv((uint32_t)p.cblocks), p.kmode, total);
+                                           FastDiv((uint32_t)p.cblocks), p.kmode, total, p.tma);
     return B2C_OK;
 }
 
@@ -259,6 +279,172 @@ TiledKernel tiled_pick(int mt, int nt) {
     return nullptr;
 }
 
+// ----------------------------------------------------------------------------- TMA path
+
+// Tensor-map encoders come from the driver through the runtime's entry-point
+// query, so the library needs no -lcuda link.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int g_trace_on = 0;
+std::once_flag g_drv_once;
+EncodeTiledFn g_enc_tiled = nullptr;
+EncodeIm2colFn g_enc_im2col = nullptr;
+int g_drv_version = 0;
+
+int load_tma_encoders() {
+    std::call_once(g_drv_once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_enc_tiled = reinterpret_cast<EncodeTiledFn>(fn);
+        fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_enc_im2col = reinterpret_cast<EncodeIm2colFn>(fn);
+        cudaDriverGetVersion(&g_drv_version);
+    });
+    if (!g_enc_tiled || !g_enc_im2col) return fail(B2C_CUDA_ERROR, "cuTensorMapEncode* not available from the driver");
+    return B2C_OK;
+}
+
+// Known driver issue (<= 13.1) with im2col maps over tensors smaller than
+// 128 KiB: clear bit 21 of the second descriptor word (the same workaround
+// CUTLASS applies, cute/atom/copy_traits_sm90_im2col.hpp).
+void im2col_small_tensor_fix(CUtensorMap* tm, size_t tensor_bytes) {
+    if (g_drv_version <= 13010 && tensor_bytes < 131072) reinterpret_cast<uint64_t*>(tm)[1] &= ~(1ull << 21);
+}
+
+int encode_im2col(CUtensorMap* tm, const b2c_conv_desc* d, const float* xh, int pix_rows) {
+    const cuuint64_t dims[4] = {(cuuint64_t)d->c, (cuuint64_t)d->w, (cuuint64_t)d->h, (cuuint64_t)d->n};
+    const cuuint64_t strides[3] = {(cuuint64_t)d->c * 4, (cuuint64_t)d->w * d->c * 4,
+                                   (cuuint64_t)d->h * d->w * d->c * 4};
+    const int lower[2] = {-d->pad, -d->pad};
+    const int upper[2] = {d->pad - (d->r - 1), d->pad - (d->r - 1)};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)d->stride, (cuuint32_t)d->stride, 1};
+    CUresult r = g_enc_im2col(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(xh), dims, strides, lower,
+                              upper, (cuuint32_t)TM_BK, (cuuint32_t)pix_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
+    im2col_small_tensor_fix(tm, (size_t)d->n * d->c * d->h * d->w * 4);
+    return B2C_OK;
+}
+
+// Row-major [rows][cols] fp32 matrix, box = 32 cols (128 B) x box_rows, SWIZZLE_128B.
+int encode_rows(CUtensorMap* tm, const float* base, long long rows, long long cols, int box_rows) {
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TM_BK, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_enc_tiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return B2C_OK;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
+}
+
+using TconvKernel = void (*)(const CUtensorMap, const CUtensorMap, TArgs);
+
+struct TconvEntry {
+    TconvKernel fn;
+    int smem;
+    int stages;
+};
+
+template <int BN, bool SWAP, int MODE>
+TconvEntry tconv_entry() {
+    return TconvEntry{&k_tconv<BN, SWAP, MODE>, TmaCfg<BN, SWAP>::SMEM, TmaCfg<BN, SWAP>::STAGES};
+}
+
+template <bool SWAP, int MODE>
+TconvEntry tconv_pick_bn(int bn) {
+    switch (bn) {
+        case 32: return tconv_entry<32, SWAP, MODE>();
+        case 64: return tconv_entry<64, SWAP, MODE>();
+        case 96: return tconv_entry<96, SWAP, MODE>();
+        case 128: return tconv_entry<128, SWAP, MODE>();
+        case 192: return tconv_entry<192, SWAP, MODE>();
+    }
+    return TconvEntry{nullptr, 0, 0};
+}
+
+TconvEntry tconv_pick(int bn, int swap, int mode) {
+    if (swap) return mode == 1 ? tconv_pick_bn<true, 1>(bn) : mode == 2 ? tconv_pick_bn<true, 2>(bn) : tconv_pick_bn<true, 0>(bn);
+    return mode == 1 ? tconv_pick_bn<false, 1>(bn) : mode == 2 ? tconv_pick_bn<false, 2>(bn) : tconv_pick_bn<false, 0>(bn);
+}
+
+int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const Geom& g, const float* x,
+            const float* w, const float* bias, float* y, void* ws, cudaStream_t st) {
+    int rc = load_tma_encoders();
+    if (rc) return rc;
+    const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
+    const int mode = p.kmode == 2 ? 1 : (plain_1x1 && t->tma == 2) ? 2 : 0;
+    TconvEntry e = tconv_pick(t->tile_n, t->swap_ab, mode);
+    if (!e.fn) return fail(B2C_INAPPLICABLE, "no TMA tcgen05 kernel for this tile");
+    rc = ensure_smem_attr((const void*)e.fn, e.smem);
+    if (rc) return rc;
+    const int pix_rows = t->swap_ab ? t->tile_n : TM_M;
+    char* wsb = reinterpret_cast<char*>(ws);
+    CUtensorMap tm_pix, tm_flt;
+    std::memset(&tm_flt, 0, sizeof(tm_flt));
+    if (mode == 0 || mode == 2) {
+        float* xh = reinterpret_cast<float*>(wsb + p.nhwc_off);
+        const int HW = d->h * d->w;
+        dim3 tgrid((HW + 31) / 32, (d->c + 31) / 32, d->n);
+        if (!(g_trace_on & 16)) {  // debug bit 4: reuse the NHWC copy already in the workspace
+            cudaError_t le = launch_pdl(k_nchw_to_nhwc, tgrid, dim3(256), 0, st, x, xh, (int)d->c, HW);
+            if (le != cudaSuccess) return cuda_fail(le, "k_nchw_to_nhwc launch");
+        }
+        rc = mode == 2 ? encode_rows(&tm_pix, xh, (long long)d->n * d->h * d->w, d->c, pix_rows)
+                       : encode_im2col(&tm_pix, d, xh, pix_rows);
+        if (rc) return rc;
+    } else {
+        rc = encode_rows(&tm_pix, x, d->n, (long long)g.K, pix_rows);
+        if (rc) return rc;
+        rc = encode_rows(&tm_flt, w, d->k, (long long)g.K, t->swap_ab ? TM_M : t->tile_n);
+        if (rc) return rc;
+    }
+    TArgs a;
+    a.g = g;
+    a.wpk = reinterpret_cast<const float*>(ws);
+    a.bias = bias;
+    a.y = y;
+    a.split = p.split;
+    a.kps = p.kps;
+    a.kblocks = p.kblocks;
+    a.fCB = FastDiv((uint32_t)p.cblocks);
+    a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
+    a.lag = std::max(0, std::min(a.drain - 2, e.stages - 1));
+    a.ws = reinterpret_cast<float*>(wsb + p.part_off);
+    a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
+    a.trace = g_trace_on & 15;
+    dim3 grid(p.grid_x, p.grid_y, p.split);
+    cudaError_t le = launch_pdl(e.fn, grid, dim3(TM_THREADS), (size_t)e.smem, st, tm_pix, tm_flt, a);
+    if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
+    return B2C_OK;
+}
+
 int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias,
              float* y, void* ws, size_t ws_bytes, cudaStream_t st) {
     std::string why;
@@ -288,10 +474,16 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
             const UmmaPlan p = umma_plan(d, t);
             UmmaEntry e = umma_pick(t->tile_n, t->swap_ab, p.kmode);
             if (!e.fn) return fail(B2C_INAPPLICABLE, "no tcgen05 kernel for this tile");
-            if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+            if (p.ws_bytes > 0 && (!ws || ws_bytes < p.ws_bytes))
+                return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
             if (!t->prepared) {
                 rc = pack_impl(d, t, w, ws, ws_bytes, st);
                 if (rc) return rc;
+            }
+            if (t->tma) {
+                rc = tma_fwd(d, t, p, g, x, w, bias, y, ws, st);
+                if (rc) return rc;
+                break;
             }
             rc = ensure_smem_attr((const void*)e.fn, e.smem);
             if (rc) return rc;
@@ -476,10 +668,19 @@ int64_t b2c_conv_bytes(const b2c_conv_desc* d) {
 int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
     (void)d;
     if (!t) return 0;
-    return (is_umma(t->variant) && !t->prepared) ? 2 : 1;
+    const int pack = (is_umma(t->variant) && !t->prepared && !(t->tma && t->variant == B2C_VAR_FC)) ? 1 : 0;
+    const int nhwc = (is_umma(t->variant) && t->tma && t->variant != B2C_VAR_FC) ? 1 : 0;
+    return 1 + pack + nhwc;
 }
 
 const char* b2c_last_error(void) { return g_last_error.c_str(); }
+
+/* Debug only (not part of include/b2conv.h): enable the phase trace of the
+ * TMA kernel's CTA 0 and read it back (256 clock64 stamps). */
+void b2c_debug_trace_enable(int on) { g_trace_on = on; }
+int b2c_debug_trace_read(long long* out) {
+    return cudaMemcpyFromSymbol(out, b2c::g_b2c_trace, sizeof(long long) * 256) == cudaSuccess ? 0 : 3;
+}
 
 const char* b2c_version(void) { return "b2conv 0.1.0 sm_100a"; }
 

@@ -251,4 +251,86 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// One lane of a converged warp returns true (elect.sync).
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, %1;\n\t"
+        "@px mov.s32 %0, 1;\n\t}"
+        : "+r"(pred)
+        : "r"(0xffffffffu));
+    return pred != 0;
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// ----------------------------------------------------------------------------
+// Phase trace (debug): CTA (0,0,0) records SM clock64 at pipeline events into a
+// device array read back by b2c_debug_trace_read(); off unless TArgs.trace != 0.
+// Slots: 0-15 phases, 16+it split saw raw_full, 48+it split arrived, 80+it MMA
+// saw raw_full, 112+it MMA saw split_full, 144+it MMA committed, 176+it TMA issued (it < 32).
+__device__ long long g_b2c_trace[256];  // single translation unit (b2conv.cu)
+#define B2C_TRACE(on, slot)                                                           \
+    do {                                                                              \
+        if ((on) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_b2c_trace[(slot)] = clock64(); \
+    } while (0)
+
+// ----------------------------------------------------------------------------
+// TMA (cp.async.bulk.tensor) and programmatic dependent launch (PDL)
+
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// im2col-mode 4-D load (tensor C,W,H,N): PixelsPerColumn output pixels in
+// raster order from (w, h, n), each contributing channelsPerPixel channels
+// from c, sampled at the filter tap offset (off_w, off_h); out-of-bounds
+// elements (the conv padding) are zero-filled by the TMA unit.
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* tmap, uint32_t bar, int c, int w,
+                                                   int h, int n, uint16_t off_w, uint16_t off_h) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(tmap), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+        : "memory");
+}
+
+// Tiled 2-D load: box at element coordinates (x innermost, y).
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(tmap), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+// PDL: let the next kernel in the stream start its prologue, and wait for the
+// previous one's results before touching global memory it may have written.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B: rows of 128 B (32 fp32
+// of K), 16-byte chunks XOR-swizzled by (row % 8) inside 1024-byte atoms of 8
+// rows (the layout TMA writes with CU_TENSOR_MAP_SWIZZLE_128B), SBO = 1024 B
+// between 8-row groups.  Successive K=8 steps add 32 B to the start address.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+    d |= (uint64_t)1 << 46;              // version (sm_100)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+
 }  // namespace b2c

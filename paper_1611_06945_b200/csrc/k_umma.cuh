@@ -230,9 +230,11 @@ __device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* acc) {
 // --------------------------------------------------------------------------- filter packing
 // packed[((t*KB + kb)*2 + part)*8*ROWS*4 + (c*ROWS + r)*4 + e] =
 //   part 0: W[oc][k], part 1: W - trunc_tf32(W), oc = t*ROWS + r, k = k-index(kb, 4c+e)
+// swz != 0 writes each (tile, K block, part) as 128-byte rows with 16-byte
+// chunks XOR-swizzled by row % 8 (the SWIZZLE_128B image k_tconv reads).
 __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __restrict__ w, float* __restrict__ out,
                                                       int rows, int kblocks, FastDiv fCB, int kmode,
-                                                      long long total) {
+                                                      long long total, int swz) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const int e = (int)(i & 3);
@@ -265,7 +267,12 @@ __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __res
             split_tf32(v, h, l);
             v = l;
         }
-        out[i] = v;
+        if (swz) {
+            const long long part_base = i - (i % (8LL * rows * 4));
+            out[part_base + ((long long)r * 8 + (c ^ (r & 7))) * 4 + e] = v;
+        } else {
+            out[i] = v;
+        }
     }
 }
 
@@ -420,6 +427,20 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_umma(UmmaArgs a) {
             if (row_ok) row_bias = __ldg(a.bias + oc);
         }
 
+        // emit with a pre-loaded bias (!SWAP: per column; SWAP: row_bias)
+        auto emit_b = [&](int col, float v, float bcol) {
+            if (!SWAP) {
+                const int oc = n0 + col;
+                if (row_ok && oc < g.OC) a.y[row_out + (long long)oc * g.PQ] = apply_act(v + bcol, g.act);
+            } else {
+                const int m = m0 + col;
+                if (row_ok && m < g.M) {
+                    uint32_t b, p;
+                    g.fPQ.divmod((uint32_t)m, b, p);
+                    a.y[((long long)b * g.OC + row_out) * g.PQ + p] = apply_act(v + row_bias, g.act);
+                }
+            }
+        };
         auto emit = [&](int col, float v) {
             if (!SWAP) {
                 const int oc = n0 + col;
@@ -436,8 +457,19 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_umma(UmmaArgs a) {
         };
 
         if (a.split == 1) {
+            // groups of 8: the 8 bias loads issue before the 8 stores (y may
+            // alias bias as far as the compiler knows)
 #pragma unroll
-            for (int j = 0; j < HALF; ++j) emit(c_begin + j, acc[j]);
+            for (int j0 = 0; j0 < HALF; j0 += 8) {
+                float bv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int oc = n0 + c_begin + j0 + j;
+                    bv[j] = SWAP ? 0.0f : (oc < g.OC ? __ldg(a.bias + oc) : 0.0f);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) emit_b(c_begin + j0 + j, acc[j0 + j], bv[j]);
+            }
         } else {
             const int tile = blockIdx.y * gridDim.x + blockIdx.x;
             float* part = a.ws + ((size_t)tile * a.split + z) * BN * UMMA_M;

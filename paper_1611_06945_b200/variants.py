@@ -53,6 +53,7 @@ class TuneParams:
     split_k: int = 1
     swap_ab: bool = False
     drain: int = 0  # K blocks per TMEM chunk before the fp32 register drain (0 = library default)
+    tma: int = 0  # tcgen05: 1 = TMA-fed kernel (im2col on an NHWC copy / 2-D tiles), 2 = 2-D tiles for 1x1; 0 = warp gathers
 
     def __post_init__(self):
         if min(self.mnt) < 1 or min(self.mnb) < 1 or self.kb < 1:
@@ -73,7 +74,8 @@ class TuneParams:
     def to_string(self) -> str:
         return (f"MNt={self.mnt[0]}:{self.mnt[1]},MNb={self.mnb[0]}:{self.mnb[1]},Kb={self.kb},vw={self.vw},"
                 f"lf={int(self.use_local_filts)},li={int(self.use_local_in)},"
-                f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)},dr={self.drain}")
+                f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)},dr={self.drain}"
+                + (f",tm={int(self.tma)}" if self.tma else ""))
 
     @staticmethod
     def from_string(text: str) -> "TuneParams":
@@ -91,6 +93,7 @@ class TuneParams:
                 split_k=int(kv.get("sk", "1")),
                 swap_ab=kv.get("sw", "0") == "1",
                 drain=int(kv.get("dr", "0")),
+                tma=int(kv.get("tm", "0")),
             )
         except (KeyError, ValueError) as e:
             raise CuclgenError(f"bad tune-params string {text!r}: {e}") from None
@@ -169,7 +172,8 @@ class Variant:
 
     def tune_struct(self, params: TuneParams) -> backend.Tune:
         return backend.Tune(self.vid, params.mnt[0], params.mnt[1], params.mnb[0], params.mnb[1], params.kb,
-                            params.vw, params.bn, 0, params.split_k, int(params.swap_ab), params.drain, 0)
+                            params.vw, params.bn, 0, params.split_k, int(params.swap_ab), params.drain, 0,
+                            int(params.tma))
 
     def applies(self, node: OpNode, edges, params: TuneParams) -> str | None:
         """None when applicable, else the reason (variants.py:206-210).  The C
@@ -244,6 +248,9 @@ class _UmmaFamily(Variant):
         split = 1
         while tiles * split * 2 <= NUM_SMS and kblocks // (split * 2) >= 4:
             split *= 2
+        p = TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=True)
+        if self.applies(node, edges, p) is None:
+            return p
         return TuneParams(bn=bn, split_k=split, swap_ab=swap)
 
     def space(self, node, edges):
@@ -258,7 +265,8 @@ class _UmmaFamily(Variant):
                 for split in (1, 2, 4, 8, 16, 32):
                     if split > 1 and kblocks // split < 2:
                         continue
-                    out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap))
+                    for tma in (True, False):
+                        out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

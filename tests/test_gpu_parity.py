@@ -52,7 +52,11 @@ def _variant_params(g):
     out = [("conv_simple", TuneParams()), ("conv_tiled", TuneParams(mnt=(4, 4), mnb=(8, 8), kb=8, vw=4)),
            ("conv_tiled", TuneParams(mnt=(2, 2), mnb=(4, 4), kb=3, vw=2))]
     for v in ("conv_umma", "conv_1x1", "conv_fc"):
-        for prm in (TuneParams(bn=32), TuneParams(bn=128, swap_ab=True), TuneParams(bn=64, split_k=2)):
+        for prm in (TuneParams(bn=32), TuneParams(bn=128, swap_ab=True), TuneParams(bn=64, split_k=2),
+                    TuneParams(bn=32, tma=True), TuneParams(bn=128, swap_ab=True, tma=True),
+                    TuneParams(bn=64, split_k=2, tma=True), TuneParams(bn=192, tma=True),
+                    TuneParams(bn=96, swap_ab=True, split_k=3, tma=True), TuneParams(bn=64, tma=2),
+                    TuneParams(bn=32, swap_ab=True, split_k=2, tma=2)):
             out.append((v, prm))
     return [(n, p) for n, p in out if VARIANTS[n].applies(node, g.edges, p) is None]
 
@@ -119,7 +123,7 @@ def test_corpus_heuristic_variant_vs_oracle(cuda, row, op):
     assert res.ok, (row, v.name, params.to_string(), res)
 
 
-@pytest.mark.parametrize("vname", ["conv_simple", "conv_tiled", "conv_umma"])
+@pytest.mark.parametrize("vname", ["conv_simple", "conv_tiled", "conv_umma", "conv_umma_tma"])
 def test_signed_inputs_relu_clips(cuda, vname):
     from paper_1611_06945_b200.variants import TuneParams
 
@@ -127,8 +131,8 @@ def test_signed_inputs_relu_clips(cuda, vname):
     g = _graph(case, True)
     x, f, b = conv_ref.conv_inputs(2, 40, 14, 14, 48, 3, "signed", low=-1.0, high=1.0)
     params = {"conv_simple": TuneParams(), "conv_tiled": TuneParams(mnt=(4, 4), mnb=(8, 8), kb=8, vw=4),
-              "conv_umma": TuneParams(bn=64)}[vname]
-    got = _run_device(g, x, f, b, vname, params)
+              "conv_umma": TuneParams(bn=64), "conv_umma_tma": TuneParams(bn=64, tma=True)}[vname]
+    got = _run_device(g, x, f, b, vname.replace("_tma", ""), params)
     plain = conv_ref.ref_conv(x, f, b, 1, 1)
     want = np.maximum(plain, 0)
     bound = 1e-5 * conv_ref.signed_bound(x, f, 1, 1) + 1e-6
@@ -145,6 +149,8 @@ def test_split_k_deterministic(cuda):
     x, f, b = conv_ref.conv_inputs(1, 384, 13, 13, 256, 3, "splitk")
     runs = [_run_device(g, x, f, b, "conv_umma", TuneParams(bn=128, split_k=8)) for _ in range(3)]
     assert all(np.array_equal(runs[0], r) for r in runs[1:])
+    runs_t = [_run_device(g, x, f, b, "conv_umma", TuneParams(bn=128, split_k=8, tma=True)) for _ in range(3)]
+    assert all(np.array_equal(runs_t[0], r) for r in runs_t[1:])
     want = conv_ref.ref_conv(x, f, b, 1, 1, relu=True)
     assert conv_ref.compare(runs[0], want, conv_ref.tolerance_for(384 * 9)).ok
 
@@ -195,7 +201,7 @@ def test_bad_args_raise(cuda):
     from paper_1611_06945_b200.errors import ShapeMismatch
 
     d = backend.make_desc(1, 3, 8, 8, 4, 3, 1, 1, 7, 8, False)  # wrong oh
-    t = backend.Tune(backend.VAR_SIMPLE, 1, 1, 1, 1, 1, 1, 32, 0, 1, 0)
+    t = backend.Tune(backend.VAR_SIMPLE, 1, 1, 1, 1, 1, 1, 32, 0, 1, 0, 0, 0, 0)
     z = torch.zeros(1024, device="cuda")
     with pytest.raises(ShapeMismatch):
         backend.fwd(d, t, z, z, z, z)
