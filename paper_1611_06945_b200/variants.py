@@ -248,7 +248,7 @@ class _UmmaFamily(Variant):
         split = 1
         while tiles * split * 2 <= NUM_SMS and kblocks // (split * 2) >= 4:
             split *= 2
-        p = TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=True)
+        p = TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=1)
         if self.applies(node, edges, p) is None:
             return p
         return TuneParams(bn=bn, split_k=split, swap_ab=swap)
@@ -265,7 +265,7 @@ class _UmmaFamily(Variant):
                 for split in (1, 2, 4, 8, 16, 32):
                     if split > 1 and kblocks // split < 2:
                         continue
-                    for tma in (True, False):
+                    for tma in (1, 2, 0):
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
         return [p for p in out if self.applies(node, edges, p) is None]
 

@@ -1,6 +1,6 @@
 #!/bin/bash
-# One GPU session: parity tests, bench, ncu launch list, ncu full capture of the dominant kernel.
-# usage (under gpurun): bash tools/gpu_round.sh [tag]
+# One GPU session: parity tests, smoke, bench, ncu launch list, ncu full captures
+# of the dominant kernel and of the top TMA kernel.   usage (under gpurun): bash tools/gpu_round.sh TAG
 set -x
 TAG=${1:-r1}
 OUT=gpurun_out/$TAG
@@ -16,6 +16,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $OUT/ncu_launch_bench.log 2>&1
 ROW=$(python -c "import json;d=json.load(open('$OUT/bench.json'));print(d['roofline']['corpus_row'])")
 BATCH=$(python -c "import json;d=json.load(open('$OUT/bench.json'));print(d['roofline']['op'].split(':in')[1].split('x')[0])")
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_(umma|tiled|simple)" -s 2 -c 1 -o $OUT/prof_dom \
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_(umma|tconv|tiled|simple|fc)" -s 2 -c 1 -o $OUT/prof_dom \
    python tools/run_op.py --row $ROW --batch $BATCH --reps 3 > $OUT/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_tconv" -s 2 -c 1 -o $OUT/prof_r42 \
+   python tools/run_op.py --row 42 --batch 20 --reps 3 > $OUT/ncu_full42.log 2>&1
 echo done

@@ -1,0 +1,112 @@
+// TMA throughput probe (B200): per-SM ingest rate of tiled 2-D boxes of various
+// shapes vs 1-D bulk copies.  Each CTA streams its own slice of a large fp32
+// matrix through a ring of shared-memory stages; prints bytes/cycle per SM.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tma_probe tools/tma_probe.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(c)); }
+__device__ __forceinline__ void expect_tx(uint32_t bar, uint32_t b) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;" ::"r"(b), "r"(bar) : "memory"); }
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t ph) {
+    asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W;\n}" ::"r"(bar), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const void* tm, uint32_t bar, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst), "l"(tm), "r"(bar), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+constexpr int STAGES = 6;
+
+// mode 0: 2-D boxes (bw cols x bh rows); mode 1: bulk copies of bw*bh*4 bytes
+__global__ void probe(const __grid_constant__ CUtensorMap tm, const float* base, int mode, int bw, int bh,
+                      int cols, int iters, long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    const uint32_t tiles = (smem_u32(smem) + 1024 + 1023) & ~1023u;
+    const uint32_t bytes = (uint32_t)bw * bh * 4;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const int tiles_x = cols / bw;
+    long long t0 = clock64();
+    for (int it = 0; it < iters + STAGES; ++it) {
+        if (it >= STAGES) mbar_wait(smem_u32(&bars[it % STAGES]), ((it / STAGES) - 1) & 1);
+        if (it < iters) {
+            const int s = it % STAGES;
+            const uint32_t bar = smem_u32(&bars[s]);
+            expect_tx(bar, bytes);
+            const int t = blockIdx.x * iters + it;  // this CTA's t-th tile
+            if (mode == 0) {
+                tma2d(tiles + s * bytes, &tm, bar, (t % tiles_x) * bw, (t / tiles_x) * bh);
+            } else {
+                bulk(tiles + s * bytes, base + (size_t)t * bw * bh, bytes, bar);
+            }
+        }
+    }
+    cycles[blockIdx.x] = clock64() - t0;
+}
+
+using EncFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+    EncFn enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+    const int rows = 16384, cols = 4096;  // 256 MB
+    float* d = nullptr;
+    cudaMalloc(&d, (size_t)rows * cols * 4);
+    cudaMemset(d, 0, (size_t)rows * cols * 4);
+    long long* cyc = nullptr;
+    cudaMalloc(&cyc, 1024 * sizeof(long long));
+    struct Cfg { int mode, bw, bh; CUtensorMapSwizzle sw; const char* name; };
+    std::vector<Cfg> cfgs = {
+        {0, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x128 SW128 (16 KB)"},
+        {0, 32, 256, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x256 SW128 (32 KB)"},
+        {0, 16, 256, CU_TENSOR_MAP_SWIZZLE_64B, "box 16x256 SW64 (16 KB)"},
+        {0, 64, 64, CU_TENSOR_MAP_SWIZZLE_NONE, "box 64x64 none (16 KB)"},
+        {0, 256, 16, CU_TENSOR_MAP_SWIZZLE_NONE, "box 256x16 none (16 KB)"},
+        {0, 4, 256, CU_TENSOR_MAP_SWIZZLE_NONE, "box 4x256 none (4 KB, 16 B rows)"},
+        {1, 32, 128, CU_TENSOR_MAP_SWIZZLE_NONE, "bulk 16 KB"},
+        {1, 32, 256, CU_TENSOR_MAP_SWIZZLE_NONE, "bulk 32 KB"},
+    };
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    for (auto& c : cfgs) {
+        CUtensorMap tm;
+        const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        const cuuint64_t str[1] = {(cuuint64_t)cols * 4};
+        const cuuint32_t box[2] = {(cuuint32_t)c.bw, (cuuint32_t)c.bh};
+        const cuuint32_t es[2] = {1, 1};
+        if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, c.sw,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            printf("%-34s encode failed\n", c.name);
+            continue;
+        }
+        const int bytes = c.bw * c.bh * 4;
+        const int smem = 2048 + STAGES * bytes;
+        for (int grid : {1, 16, 148}) {
+            const long long total_tiles = (long long)rows * cols * 4 / bytes;
+            int iters = (int)std::min<long long>(total_tiles / grid, 2048);
+            for (int rep = 0; rep < 2; ++rep) probe<<<grid, 32, smem>>>(tm, d, c.mode, c.bw, c.bh, cols, iters, cyc);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            std::vector<long long> h(grid);
+            cudaMemcpy(h.data(), cyc, grid * 8, cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (auto v : h) mx = v > mx ? v : mx;
+            printf("%-34s grid %3d: %6.1f B/clk/SM  (%d tiles/CTA, %lld cyc)\n", c.name, grid,
+                   (double)iters * bytes / mx, iters, mx);
+        }
+    }
+    return 0;
+}
