@@ -1,41 +1,62 @@
-// TMA-fed tcgen05 / TMEM implicit-GEMM convolution, fp32-exact via 3xTF32.
+// TMA-fed, persistent tcgen05 / TMEM implicit-GEMM convolution, fp32-exact
+// via 3xTF32.
 //
-// Same GEMM view and precision scheme as k_umma (cuclgen/variants.py:376-414
-// ConvTiled's M = img*oy*ox, N = out_chan, K = in_chan*ksz*ksz; fused
-// bias/ReLU epilogue of variants.py:160-165), but no thread ever gathers an
-// operand element from global memory:
+// GEMM view of the reference ConvTiled (cuclgen/variants.py:376-414):
+// M = img*oy*ox output pixels, N = out_chan, K = in_chan*ksz*ksz, with the
+// bias/ReLU epilogue of variants.py:160-165 fused (graphopt.fuse_activations,
+// graphopt.py:59-86).  No thread gathers an operand element from global
+// memory; the TMA unit does, straight into the layout the tensor core reads:
 //
 //   * MODE 0 (conv): the activations are re-laid out once per call to NHWC
-//     (k_nchw_to_nhwc, the B200 form of the reference's required_formats
+//     (k_nchw_to_nhwc: the B200 form of the reference's required_formats
 //     conversion, variants.py:416-424 / runner.py:96-105, charged to the op)
 //     and one TMA *im2col* load per K block brings 128 (or BN) output pixels x
-//     32 channels of one filter tap straight into the K-major SWIZZLE_128B
-//     layout the tensor core reads; the TMA unit zero-fills the padding.
-//     Filters are packed once (cached) into the same swizzled layout, raw and
-//     lo halves, and streamed with one cp.async.bulk per K block.
+//     32 channels of one filter tap into the K-major SWIZZLE_128B layout; the
+//     TMA unit zero-fills the conv padding.  Filters are packed once (cached,
+//     b2c_conv_prepare) into the same swizzled layout, raw and lo halves, and
+//     streamed with one cp.async.bulk per K block.
 //   * MODE 2 (1x1, stride 1, no pad; conv_1x1, variants.py:279-325): the NHWC
-//     copy is a plain [pixels][C] matrix, so a 2-D tiled TMA box replaces
-//     the im2col walk (filters as in MODE 0).
+//     copy is a plain [pixels][C] matrix; a 2-D tiled box replaces the im2col.
+//   * MODE 3 (first layers, C <= 4: AlexNet/NiN conv1, GoogLeNet conv1): NHWC
+//     with C padded to 4; a K block is 8 filter taps x 4 channels, loaded as 8
+//     im2col boxes of 16-byte pixels into the no-swizzle core-matrix layout
+//     [tap][row][16 B] (strides 4 and 2 are the TMA element strides).
+//   * MODE 4 (first layers, C <= 4, default): x is copied to a zero-padded
+//     NHWC buffer with 4 channels; for one filter row ky, the 8 x-taps x 4
+//     channels an output pixel needs are 32 consecutive floats there (128 B).
+//     A 5-D tiled tensor map with overlapping strides (window, ox step S*16 B,
+//     oy step S rows, ky step 1 row, image) loads a BX x BY block of output
+//     pixels x 32 window floats per box into the SWIZZLE_128B layout: 128-byte
+//     rows instead of MODE 3's 16-byte ones (the TMA unit issues ~0.75 rows
+//     per clock per SM, so row width sets its throughput).
 //   * MODE 1 (fc, variants.py:328-373): the whole-image filter makes both
 //     operands plain row-major [rows][K] matrices (x as [img][ic*h*w], w as
-//     [oc][ic*h*w]); both are loaded raw by 2-D tiled TMA, so the 151 MB fc6
-//     weight tensor is read from HBM exactly once, with no pack.
+//     [oc][ic*h*w]), loaded raw by 2-D tiled TMA: the fc6 weights (151 MB)
+//     are read from HBM once, with no pack.
 //
-// Warp roles (320 threads):
-//   warps 0-7  split + drain + epilogue.  All 256 threads take every stage
-//              (each its 1/256 of the tile; a group that ran ahead over
-//              alternate stages could see a stale mbarrier parity, since TMA
-//              loads may land out of order): they wait for the TMA bytes, write
-//              lo = x - trunc_tf32(x) beside every raw operand the TMA loaded
-//              (elementwise on the swizzled tile, so no index math), and
-//              drain finished TMEM chunks into fp32 register sums (the
-//              accumulation-precision scheme of k_umma.cuh).
-//   warp 8     TMEM allocation; lane 0 issues 12 tcgen05.mma.kind::tf32 per
-//              K block (4 K=8 steps x {hi*hi, hi*lo, lo*hi}).
-//   warp 9     lane 0 issues the TMA / bulk loads.
-// Kernels are launched with programmatic dependent launch: the prologue
-// (barrier init, TMEM alloc, tensor-map prefetch) overlaps the previous
-// kernel's tail; griddepcontrol.wait precedes every global access.
+// Precision (see k_umma.cuh): kind::tf32 truncates an fp32 operand to TF32,
+// so raw x is the "hi" operand and lo = x - trunc_tf32(x);
+// D += Ahi*Bhi + Ahi*Blo + Alo*Bhi.  K is accumulated in TMEM chunks of
+// `drain` K blocks into two ping-ponged slots and each finished chunk is
+// drained into fp32 round-to-nearest register sums, bounding the tensor
+// core's truncating accumulation error for any K.
+//
+// Persistent: grid = min(work units, SMs); a unit is (pixel tile, filter
+// tile, K split).  The smem ring, the TMEM slots and all barrier phases run
+// on across units, so the epilogue of one unit overlaps the main loop of the
+// next and the pipeline never drains between tiles.
+//
+// Warp roles:
+//   warps 0-3        split: for every stage, lo = x - trunc(x) beside each raw
+//                    operand the TMA loaded (elementwise on the tile image).
+//   warps 4..4+4DG-1 drain + epilogue (DG = 1, or 2 column halves for BN > 128):
+//                    tcgen05.ld finished chunks, fp32 sums, + bias, ReLU,
+//                    NCHW stores (or split-K partials + deterministic reduce).
+//   next warp        TMEM allocation; one lane issues 12 tcgen05.mma per K block.
+//   last warp        one lane issues the TMA / bulk loads.
+// Launched with programmatic dependent launch: the prologue (barrier init,
+// TMEM alloc, tensor-map prefetch) overlaps the previous kernel;
+// griddepcontrol.wait precedes every global access.
 #pragma once
 #include <cuda.h>
 
@@ -45,18 +66,21 @@
 namespace b2c {
 
 constexpr int TM_M = 128;
-constexpr int TM_BK = 32;                 // fp32 K elements per stage (128-byte rows)
-constexpr int TM_SPLIT = 256;             // split / drain / epilogue threads (warps 0-7)
-constexpr int TM_MMA_WARP = 8;
-constexpr int TM_LOAD_WARP = 9;
-constexpr int TM_THREADS = 320;
-constexpr int TM_HDR = 256;               // barriers, TMEM slot, flags
-constexpr int TM_BIAS = 1024;             // bias of the tile's out_chans (<= 256 floats)
-constexpr int TM_MAX_SMEM = 232448;       // 227 KB opt-in per CTA
+constexpr int TM_BK = 32;              // fp32 K elements per stage
+constexpr int TM_SPLIT_THREADS = 128;  // warps 0-3
+constexpr int TM_HDR = 2048;           // barriers, TMEM slot, flags (< 1 KB); unit bias at +1 KB (<= 256 floats)
+constexpr int TM_MAX_SMEM = 232448;    // 227 KB opt-in per CTA
+constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 
-template <int BN, bool SWAP>
+template <int BN, bool SWAP, int MODE>
 struct TmaCfg {
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
+    static constexpr int DG = BN > 128 ? 2 : 1;  // drain warp groups (column halves)
+    static constexpr int DRAIN_COLS = BN / DG;
+    static constexpr int DRAIN_THREADS = 128 * DG;
+    static constexpr int MMA_WARP = 4 + 4 * DG;
+    static constexpr int LOAD_WARP = MMA_WARP + 1;
+    static constexpr int THREADS = 32 * (LOAD_WARP + 1);
     static constexpr int A_ROWS = TM_M;
     static constexpr int B_ROWS = BN;
     static constexpr int PIX_ROWS = SWAP ? B_ROWS : A_ROWS;
@@ -66,34 +90,69 @@ struct TmaCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_BYTES : 0;  // raw part; lo follows at + PIX_ROWS*128
     static constexpr int FLT_OFF = SWAP ? 0 : A_BYTES;
-    static constexpr int BUDGET = TM_MAX_SMEM - TM_HDR - TM_BIAS - 1024;
+    static constexpr int FLT_STAGE = 2 * FLT_ROWS * 128;  // packed filters per K block (raw | lo)
+    static constexpr int BUDGET = TM_MAX_SMEM - TM_HDR - 1024;
     static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
-    static constexpr int SMEM = TM_HDR + TM_BIAS + 1024 + STAGES * STAGE_BYTES;
+    static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-    static constexpr int HALF = BN / 2;
+    static constexpr bool SW128 = MODE != 3;
+    static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
+    static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
     static_assert(STAGES >= 2, "need at least two stages");
-    static_assert(HALF % 8 == 0, "TMEM drain granularity");
+    static_assert(DRAIN_COLS % 8 == 0, "TMEM drain granularity");
 };
 
 struct TArgs {
     Geom g;
-    const float* wpk;   // MODE 0: packed filters [flt tile][K block][raw | lo][rows][128 B swizzled]
+    const float* wpk;   // packed filters [flt tile][K block][raw | lo][rows][128 B]
     const float* bias;
     float* y;
-    float* ws;          // split-K partials [tiles][split][BN][128]
-    int* sems;          // split-K tickets [tiles], zero at rest
+    float* ws;          // split-K partials [tile][split][BN][128]
+    int* sems;          // split-K tickets [tile], zero at rest
     int split, kps, kblocks;
+    int tiles_n;        // filter tiles
+    int units;          // pixel tiles * filter tiles * split
+    int bx, by;         // MODE 4: output-pixel block of a tile (bx * by <= 128 rows)
+    int tiles_x, tiles_y;  // MODE 4: blocks per image row / column
     FastDiv fCB;        // MODE 0: channel blocks of 32 per filter tap
-    int drain, lag;
-    int trace;          // debug: record phase clocks of CTA 0 into g_b2c_trace
+    int drain;
+    int trace;          // debug: phase clocks of CTA 0 into g_b2c_trace
 };
+
+struct Unit {
+    int t, m0, n0, z, kb_begin, nkb;
+    int b, oy0, ox0;  // MODE 4 tile origin
+};
+
+template <int PIX_ROWS, int FLT_ROWS, int MODE>
+__device__ __forceinline__ Unit unit_of(const TArgs& a, int u) {
+    Unit w;
+    w.z = u % a.split;
+    w.t = u / a.split;
+    const int nt = w.t % a.tiles_n, mt = w.t / a.tiles_n;
+    w.m0 = mt * PIX_ROWS;
+    w.n0 = nt * FLT_ROWS;
+    w.kb_begin = w.z * a.kps;
+    w.nkb = min(a.kblocks, w.kb_begin + a.kps) - w.kb_begin;
+    if (MODE == 4) {
+        const int per_img = a.tiles_x * a.tiles_y;
+        w.b = mt / per_img;
+        const int r = mt - w.b * per_img;
+        w.oy0 = (r / a.tiles_x) * a.by;
+        w.ox0 = (r % a.tiles_x) * a.bx;
+    } else {
+        w.b = w.oy0 = w.ox0 = 0;
+    }
+    return w;
+}
 
 // ----------------------------------------------------------------------------- NCHW -> NHWC
 
-// x [N][C][HW] -> xh [N][HW][C]; 32x32 tiles through shared memory so both the
-// read (along pixels) and the write (along channels) are coalesced.
+// x [N][C][HW] -> xh [N][HW][Cp] (Cp >= C, channels C..Cp-1 zero); 32x32 tiles
+// through shared memory so the read (along pixels) and the write (along
+// channels) are both coalesced.
 __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ x, float* __restrict__ xh, int C,
-                                                      int HW) {
+                                                      int Cp, int HW) {
     __shared__ float tile[32][33];
     pdl_launch_dependents();
     pdl_wait();
@@ -101,7 +160,7 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
     const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const float* src = x + (size_t)n * C * HW;
-    float* dst = xh + (size_t)n * HW * C;
+    float* dst = xh + (size_t)n * HW * Cp;
 #pragma unroll
     for (int j = ty; j < 32; j += 8) {
         const int c = c0 + j, p = p0 + tx;
@@ -111,45 +170,163 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
 #pragma unroll
     for (int j = ty; j < 32; j += 8) {
         const int p = p0 + j, c = c0 + tx;
-        if (p < HW && c < C) dst[(size_t)p * C + c] = tile[tx][j];
+        if (p < HW && c < Cp) dst[(size_t)p * Cp + c] = tile[tx][j];
     }
 }
 
-// ----------------------------------------------------------------------------- split-K
-// Write this CTA's fp32 partial tile; returns true in the CTA that arrives
-// last for its output tile (it then reduces all partials in split order, so
-// the result is deterministic).  Called by all 256 split/epilogue threads.
-template <int BN>
-__device__ __forceinline__ bool split_reduce_last(const TArgs& a, const float* acc, int c_begin, int row, int z,
-                                                  int* last_flag) {
-    constexpr int HALF = BN / 2;
-    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-    float* part = a.ws + ((size_t)tile * a.split + z) * BN * TM_M;
+// x [N][C][H][W] (C <= 4) -> xp [N][Hp][Wp][4], image at (pad, pad), zeros
+// elsewhere: one thread per padded pixel, coalesced plane reads, float4 writes.
+__global__ void __launch_bounds__(256) k_to_nhwc4_pad(const float* __restrict__ x, float4* __restrict__ xp, int C,
+                                                      int H, int W, int Hp, int Wp, int pad, long long total) {
+    pdl_launch_dependents();
+    pdl_wait();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int xq = (int)(i % Wp);
+        const long long t = i / Wp;
+        const int yq = (int)(t % Hp);
+        const int b = (int)(t / Hp);
+        const int iy = yq - pad, ix = xq - pad;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if ((unsigned)iy < (unsigned)H && (unsigned)ix < (unsigned)W) {
+            const float* src = x + ((size_t)b * C * H + iy) * W + ix;
 #pragma unroll
-    for (int j = 0; j < HALF; ++j) __stcg(part + (size_t)(c_begin + j) * TM_M + row, acc[j]);
-    __threadfence();
-    named_bar_sync(1, TM_SPLIT);
-    if (threadIdx.x == 0) {
-        const int ticket = atomicAdd(a.sems + tile, 1);
-        *last_flag = (ticket == a.split - 1);
+            for (int c = 0; c < 4; ++c)
+                if (c < C) v[c] = __ldg(src + (size_t)c * H * W);
+        }
+        xp[i] = make_float4(v[0], v[1], v[2], v[3]);
     }
-    named_bar_sync(1, TM_SPLIT);
-    const bool last = *last_flag != 0;
-    if (last) {
+}
+
+// ----------------------------------------------------------------------------- split + epilogue helpers
+
+// lo = x - trunc_tf32(x) for a raw operand image of `rows` x 128 B, written
+// beside it (at + rows*128).  Elementwise on the image, so the swizzle / core
+// matrix layout needs no index math.  128 split threads.
+template <int ROWS>
+__device__ __forceinline__ void split_tile(uint32_t raw, int tid) {
+    const uint32_t lo = raw + (uint32_t)ROWS * 128u;
+#pragma unroll
+    for (int k = 0; k < ROWS * 8 / TM_SPLIT_THREADS; ++k) {
+        const uint32_t off = (uint32_t)(tid + k * TM_SPLIT_THREADS) * 16u;
+        const float4 v = lds128(raw + off);
+        float h, l0, l1, l2, l3;
+        split_tf32(v.x, h, l0);
+        split_tf32(v.y, h, l1);
+        split_tf32(v.z, h, l2);
+        split_tf32(v.w, h, l3);
+        sts128(lo + off, l0, l1, l2, l3);
+    }
+}
+
+// One unit's output: + bias, ReLU (variants.py:160-165), NCHW stores; with
+// split-K, the fp32 partial goes to the workspace and the unit that arrives
+// last for its tile (atomic ticket) reduces all partials in split order, so
+// results are deterministic.  Called by the NT drain threads; `row` is this
+// thread's TMEM lane (MMA M row), columns c_begin .. c_begin+DC.
+template <int BN, bool SWAP, int DC, int NT, int MODE>
+__device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, float* acc, int c_begin, int row,
+                                              int dtid, int* last_flag, float* bias_s, float bpre) {
+    const Geom& g = a.g;
+    if (!SWAP) {  // the unit's out_chan biases -> smem (bpre was loaded by thread dtid before the drains)
+        named_bar_sync(1, NT);  // previous unit's readers are done
+        if (dtid < BN) bias_s[dtid] = bpre;
+        named_bar_sync(1, NT);
+    }
+    if (a.split > 1) {
+        float* part = a.ws + ((size_t)w.t * a.split + w.z) * BN * TM_M;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) __stcg(part + (size_t)(c_begin + j) * TM_M + row, acc[j]);
         __threadfence();
-        if (threadIdx.x == 0) a.sems[tile] = 0;
+        named_bar_sync(1, NT);
+        if (dtid == 0) {
+            const int ticket = atomicAdd(a.sems + w.t, 1);
+            *last_flag = (ticket == a.split - 1);
+        }
+        named_bar_sync(1, NT);
+        const bool last = *last_flag != 0;
+        named_bar_sync(1, NT);  // last_flag is rewritten by the next unit
+        if (!last) return;
+        __threadfence();
+        if (dtid == 0) a.sems[w.t] = 0;
+        const float* base = a.ws + (size_t)w.t * a.split * BN * TM_M;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
+        for (int zz = 0; zz < a.split; ++zz) {
+#pragma unroll
+            for (int j = 0; j < DC; ++j) acc[j] += __ldcg(base + ((size_t)zz * BN + c_begin + j) * TM_M + row);
+        }
     }
-    return last;
+    float* __restrict__ yp = a.y;
+    if (!SWAP) {  // row = output pixel, columns = out_chans
+        long long row_out;
+        if (MODE == 4) {  // rectangular tile: row = y * bx + x
+            const int y = row / a.bx, x = row - (row / a.bx) * a.bx;
+            const int oy = w.oy0 + y, ox = w.ox0 + x;
+            if (y >= a.by || oy >= g.OH || ox >= g.OW) return;
+            row_out = (long long)w.b * g.OC * g.PQ + (long long)oy * g.OW + ox;
+        } else {
+            const int m = w.m0 + row;
+            if (m >= g.M) return;
+            uint32_t b, p;
+            g.fPQ.divmod((uint32_t)m, b, p);
+            row_out = (long long)b * g.OC * g.PQ + p;
+        }
+        // pass 1: + bias (vector smem loads), ReLU; pass 2: stores only, one
+        // 64-bit pointer step per out_chan plane (no loads between stores)
+        const int act = g.act;
+#pragma unroll
+        for (int j = 0; j < DC; j += 4) {
+            const float4 bq = *reinterpret_cast<const float4*>(bias_s + c_begin + j);
+            acc[j] = apply_act(acc[j] + bq.x, act);
+            acc[j + 1] = apply_act(acc[j + 1] + bq.y, act);
+            acc[j + 2] = apply_act(acc[j + 2] + bq.z, act);
+            acc[j + 3] = apply_act(acc[j + 3] + bq.w, act);
+        }
+        float* yr = yp + row_out + (long long)(w.n0 + c_begin) * g.PQ;
+        const long long pq = g.PQ;
+        const int nvalid = min(DC, g.OC - (w.n0 + c_begin));
+        if (nvalid >= DC) {
+#pragma unroll
+            for (int j = 0; j < DC; ++j, yr += pq) *yr = acc[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < DC; ++j, yr += pq)
+                if (j < nvalid) *yr = acc[j];
+        }
+    } else {  // row = out_chan, columns = output pixels
+        const int oc = w.n0 + row;
+        if (oc >= g.OC) return;
+        const float rb = __ldg(a.bias + oc);
+        const int act = g.act;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) acc[j] = apply_act(acc[j] + rb, act);
+        const int m_begin = w.m0 + c_begin;
+        uint32_t b, p;
+        g.fPQ.divmod((uint32_t)min(m_begin, g.M - 1), b, p);
+        float* yr = yp + ((long long)b * g.OC + oc) * g.PQ + p;  // walks pixels, hopping images at PQ
+        const long long img_hop = (long long)(g.OC - 1) * g.PQ;
+        int pp = (int)p;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            if (m_begin + j < g.M) *yr = acc[j];
+            ++yr;
+            if (++pp == g.PQ) {
+                pp = 0;
+                yr += img_hop;
+            }
+        }
+    }
 }
 
 // ----------------------------------------------------------------------------- main kernel
 
 template <int BN, bool SWAP, int MODE>
-__global__ void __launch_bounds__(TM_THREADS, 1)
+__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
     k_tconv(const __grid_constant__ CUtensorMap tm_pix, const __grid_constant__ CUtensorMap tm_flt, TArgs a) {
-    using Cfg = TmaCfg<BN, SWAP>;
+    using Cfg = TmaCfg<BN, SWAP, MODE>;
     constexpr int STAGES = Cfg::STAGES;
-    constexpr int HALF = Cfg::HALF;
+    constexpr int DC = Cfg::DRAIN_COLS;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* split_full = raw_full + STAGES;
@@ -158,37 +335,29 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     uint64_t* tempty_bar = tfull_bar + 2;      // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-    float* bias_s = reinterpret_cast<float*>(smem + TM_HDR);
-    const uint32_t tiles_u32 = (smem_u32(smem) + TM_HDR + TM_BIAS + 1023u) & ~1023u;
+    float* bias_s = reinterpret_cast<float*>(smem + 1024);
+    const uint32_t tiles_u32 = (smem_u32(smem) + TM_HDR + 1023u) & ~1023u;
 
     const Geom& g = a.g;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) B2C_TRACE(a.trace, 0);
-
-    const int m0 = blockIdx.x * Cfg::PIX_ROWS;
-    const int n0 = blockIdx.y * Cfg::FLT_ROWS;
-    const int z = blockIdx.z;
-    const int kb_begin = z * a.kps;
-    const int kb_end = min(a.kblocks, kb_begin + a.kps);
-    const int nkb = kb_end - kb_begin;
     const int G = a.drain;
-    const int nchunks = (nkb + G - 1) / G;
+    if (tid == 0) B2C_TRACE(a.trace, 0);
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&raw_full[s]), 1);
-            mbar_init(smem_u32(&split_full[s]), TM_SPLIT);
+            mbar_init(smem_u32(&split_full[s]), TM_SPLIT_THREADS);
             mbar_init(smem_u32(&empty_bar[s]), 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull_bar[s]), 1);
-            mbar_init(smem_u32(&tempty_bar[s]), TM_SPLIT);
+            mbar_init(smem_u32(&tempty_bar[s]), Cfg::DRAIN_THREADS);
         }
         mbar_fence_init();
     }
-    if (warp == TM_MMA_WARP) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
-    if (warp == TM_LOAD_WARP && lane == 0) {
+    if (warp == Cfg::MMA_WARP) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    if (warp == Cfg::LOAD_WARP && lane == 0) {
         tma_prefetch_desc(&tm_pix);
         if (MODE == 1) tma_prefetch_desc(&tm_flt);
     }
@@ -199,232 +368,194 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     if (tid == 0) B2C_TRACE(a.trace, 1);
     pdl_launch_dependents();
     pdl_wait();
-    if (tid == 0) B2C_TRACE(a.trace, 2);
 
-    if (warp < TM_MMA_WARP) {
-        // ------------------------------------------------------------ split + drain + epilogue
-        const int gtid = tid;
-        const int quarter = warp & 3, half = warp >> 2;
-        const int c_begin = half * HALF;
-        const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c_begin;
-        float acc[HALF];
-#pragma unroll
-        for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
-        if (!SWAP && tid < BN) {  // the tile's out_chan biases, read by the epilogue from smem
-            const int oc = n0 + tid;
-            bias_s[tid] = oc < g.OC ? __ldg(a.bias + oc) : 0.0f;
-        }
-
-        auto drain_chunk = [&](int c) {
-            const int slot = c & 1;
-            mbar_wait(smem_u32(&tfull_bar[slot]), (uint32_t)(c >> 1) & 1u);
-            tc_fence_after();
-            tmem_add_cols<HALF>(t_row + (uint32_t)(slot * BN), acc);
-            tc_fence_before();
-            mbar_arrive(smem_u32(&tempty_bar[slot]));
-        };
-        auto split_region = [&](uint32_t raw, int rows) {
-            const uint32_t lo = raw + (uint32_t)rows * 128u;
-            for (int i = gtid; i < rows * 8; i += TM_SPLIT) {
-                const float4 v = lds128(raw + (uint32_t)i * 16u);
-                float h, l0, l1, l2, l3;
-                split_tf32(v.x, h, l0);
-                split_tf32(v.y, h, l1);
-                split_tf32(v.z, h, l2);
-                split_tf32(v.w, h, l3);
-                sts128(lo + (uint32_t)i * 16u, l0, l1, l2, l3);
+    if (warp < 4) {
+        // ------------------------------------------------------------ split
+        int stage = 0, n = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+            for (int i = 0; i < w.nkb; ++i, ++n) {
+                const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
+                mbar_wait(smem_u32(&raw_full[stage]), phase);
+                if (tid == 0 && n < 32) B2C_TRACE(a.trace, 16 + n);
+                if (!(a.trace & 4)) {  // debug bit 2: skip the split (timing experiments only)
+                    split_tile<Cfg::PIX_ROWS>(sbase + Cfg::PIX_OFF, tid);
+                    if (MODE == 1) split_tile<Cfg::FLT_ROWS>(sbase + Cfg::FLT_OFF, tid);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(smem_u32(&split_full[stage]));
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
             }
-        };
-
-        int drained = 0;
-        for (int it = 0; it < nkb; ++it) {
-            while (drained < nchunks && it >= (drained + 1) * G + a.lag) drain_chunk(drained++);
-            const int stage = it % STAGES;
-            const uint32_t phase = (uint32_t)(it / STAGES) & 1u;
-            const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
-            mbar_wait(smem_u32(&raw_full[stage]), phase);
-            if (gtid == 0 && it < 32) B2C_TRACE(a.trace, 16 + it);
-            if (!(a.trace & 4)) {  // debug bit 2: skip the split (timing experiments only)
-                split_region(sbase + Cfg::PIX_OFF, Cfg::PIX_ROWS);
-                if (MODE == 1) split_region(sbase + Cfg::FLT_OFF, Cfg::FLT_ROWS);
-            }
-            fence_proxy_async_smem();
-            mbar_arrive(smem_u32(&split_full[stage]));
-            if (gtid == 0 && it < 32) B2C_TRACE(a.trace, 48 + it);
         }
-        while (drained < nchunks) drain_chunk(drained++);
-        if (tid == 0) B2C_TRACE(a.trace, 4);
-
-        // ------------------------------------------------------------ epilogue
-        // Values are produced in groups of 8 columns (bias from smem first), so
-        // no global load sits between the stores.
-        float* __restrict__ yp = a.y;
+    } else if (warp < Cfg::MMA_WARP) {
+        // ------------------------------------------------------------ drain + epilogue
+        const int dw = warp - 4;
+        const int quarter = dw & 3;  // TMEM lane quarter = warp % 4
+        const int c_begin = (dw >> 2) * DC;
+        const int dtid = tid - 128;
         const int row = quarter * 32 + lane;  // TMEM lane = MMA M row
-        named_bar_sync(2, TM_SPLIT);      // bias_s visible
-        if (!SWAP) {
-            const int m = m0 + row;
-            const bool row_ok = m < g.M;
-            long long row_out = 0;
-            if (row_ok) {
-                uint32_t b, p;
-                g.fPQ.divmod((uint32_t)m, b, p);
-                row_out = (long long)b * g.OC * g.PQ + p;
+        const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c_begin;
+        int cidx = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+            float acc[DC];
+#pragma unroll
+            for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
+            float bpre = 0.0f;  // this thread's share of the unit's biases, loaded under the main loop
+            if (!SWAP && dtid < BN && w.n0 + dtid < g.OC) bpre = __ldg(a.bias + w.n0 + dtid);
+            const int nch = (w.nkb + G - 1) / G;
+            for (int c = 0; c < nch; ++c, ++cidx) {
+                const int slot = cidx & 1;
+                mbar_wait(smem_u32(&tfull_bar[slot]), (uint32_t)(cidx >> 1) & 1u);
+                tc_fence_after();
+                tmem_add_cols<DC>(t_row + (uint32_t)(slot * BN), acc);
+                tc_fence_before();
+                mbar_arrive(smem_u32(&tempty_bar[slot]));
             }
-            auto store8 = [&](int c0, const float* v) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int oc = n0 + c0 + j;
-                    if (row_ok && oc < g.OC) yp[row_out + (long long)oc * g.PQ] = apply_act(v[j] + bias_s[c0 + j], g.act);
-                }
-            };
-            if (a.split == 1) {
-#pragma unroll
-                for (int j0 = 0; j0 < HALF; j0 += 8) store8(c_begin + j0, acc + j0);
-            } else if (split_reduce_last<BN>(a, acc, c_begin, row, z, last_flag)) {
-                const float* __restrict__ base = a.ws + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * a.split * BN * TM_M;
-#pragma unroll 1
-                for (int j0 = 0; j0 < HALF; j0 += 8) {
-                    float v[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) v[j] = 0.f;
-                    for (int zz = 0; zz < a.split; ++zz)
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) v[j] += __ldcg(base + ((size_t)zz * BN + c_begin + j0 + j) * TM_M + row);
-                    store8(c_begin + j0, v);
-                }
-            }
-        } else {
-            const int oc = n0 + row;
-            const bool row_ok = oc < g.OC;
-            const float rb = row_ok ? __ldg(a.bias + oc) : 0.0f;
-            auto store8 = [&](int c0, const float* v) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int m = m0 + c0 + j;
-                    if (row_ok && m < g.M) {
-                        uint32_t b, p;
-                        g.fPQ.divmod((uint32_t)m, b, p);
-                        yp[((long long)b * g.OC + oc) * g.PQ + p] = apply_act(v[j] + rb, g.act);
-                    }
-                }
-            };
-            if (a.split == 1) {
-#pragma unroll
-                for (int j0 = 0; j0 < HALF; j0 += 8) store8(c_begin + j0, acc + j0);
-            } else if (split_reduce_last<BN>(a, acc, c_begin, row, z, last_flag)) {
-                const float* __restrict__ base = a.ws + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * a.split * BN * TM_M;
-#pragma unroll 1
-                for (int j0 = 0; j0 < HALF; j0 += 8) {
-                    float v[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) v[j] = 0.f;
-                    for (int zz = 0; zz < a.split; ++zz)
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) v[j] += __ldcg(base + ((size_t)zz * BN + c_begin + j0 + j) * TM_M + row);
-                    store8(c_begin + j0, v);
-                }
-            }
+            if (dtid == 0 && u == (int)blockIdx.x) B2C_TRACE(a.trace, 4);
+            const int ui = (u - (int)blockIdx.x) / (int)gridDim.x;
+            if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 208 + 2 * ui);
+            epilogue_unit<BN, SWAP, DC, Cfg::DRAIN_THREADS, MODE>(a, w, acc, c_begin, row, dtid, last_flag, bias_s, bpre);
+            if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 209 + 2 * ui);
         }
-    } else if (warp == TM_MMA_WARP) {
+        if (dtid == 0) B2C_TRACE(a.trace, 6);
+    } else if (warp == Cfg::MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer (whole warp waits, one lane issues)
         constexpr uint32_t idesc = umma_idesc(2, TM_M, BN);
-        int stage = 0, kin = 0, cidx = 0;
+        int stage = 0, cidx = 0, n = 0;
         uint32_t phase = 0;
-        for (int it = 0; it < nkb; ++it) {
-            const int slot = cidx & 1;
-            const bool first = kin == 0;
-            const bool last = (kin == G - 1) || (it == nkb - 1);
-            if (first && cidx >= 2) {
-                mbar_wait(smem_u32(&tempty_bar[slot]), (uint32_t)((cidx >> 1) - 1) & 1u);
-                tc_fence_after();
-            }
-            if (lane == 0 && it < 32) B2C_TRACE(a.trace, 80 + it);
-            // split_full is armed by the split threads only after they observed
-            // raw_full, so it also covers the TMA / bulk bytes.
-            mbar_wait(smem_u32(&split_full[stage]), phase);
-            tc_fence_after();
-            if (lane == 0 && it < 32) B2C_TRACE(a.trace, 112 + it);
-            if (elect_one_sync()) {
-                const uint32_t a_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
-                const uint32_t a_lo = a_raw + TM_M * 128;
-                const uint32_t b_raw = a_raw + Cfg::A_BYTES;
-                const uint32_t b_lo = b_raw + BN * 128;
-                const uint32_t d = tmem_base + (uint32_t)(slot * BN);
-#pragma unroll
-                for (int s = 0; s < TM_BK / 8; ++s) {
-                    const uint64_t dah = umma_desc_sw128(a_raw + s * 32);
-                    const uint64_t dal = umma_desc_sw128(a_lo + s * 32);
-                    const uint64_t dbh = umma_desc_sw128(b_raw + s * 32);
-                    const uint64_t dbl = umma_desc_sw128(b_lo + s * 32);
-                    mma_tf32(d, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
-                    if (!(a.trace & 2)) {  // debug bit 1: hi*hi only (timing experiments only)
-                        mma_tf32(d, dah, dbl, idesc, 1u);
-                        mma_tf32(d, dal, dbh, idesc, 1u);
-                    }
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+            int kin = 0;
+            for (int i = 0; i < w.nkb; ++i, ++n) {
+                const int slot = cidx & 1;
+                const bool first = kin == 0;
+                const bool last = (kin == G - 1) || (i == w.nkb - 1);
+                if (first && cidx >= 2) {
+                    mbar_wait(smem_u32(&tempty_bar[slot]), (uint32_t)((cidx >> 1) - 1) & 1u);
+                    tc_fence_after();
                 }
-                tc_commit(smem_u32(&empty_bar[stage]));
-                if (last) tc_commit(smem_u32(&tfull_bar[slot]));
-                if (it < 32) B2C_TRACE(a.trace, 144 + it);
-            }
-            __syncwarp();
-            if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1u;
-            }
-            if (++kin == G) {
-                kin = 0;
-                ++cidx;
+                // split_full is armed only after the split threads observed
+                // raw_full, so it also covers the TMA / bulk bytes.
+                mbar_wait(smem_u32(&split_full[stage]), phase);
+                tc_fence_after();
+                if (lane == 0 && n < 32) B2C_TRACE(a.trace, 112 + n);
+                if (elect_one_sync()) {
+                    const uint32_t a_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
+                    const uint32_t a_lo = a_raw + TM_M * 128;
+                    const uint32_t b_raw = a_raw + Cfg::A_BYTES;
+                    const uint32_t b_lo = b_raw + BN * 128;
+                    const uint32_t d = tmem_base + (uint32_t)(slot * BN);
+#pragma unroll
+                    for (int s = 0; s < TM_BK / 8; ++s) {
+                        uint64_t dah, dal, dbh, dbl;
+                        if (Cfg::SW128) {
+                            dah = umma_desc_sw128(a_raw + s * 32);
+                            dal = umma_desc_sw128(a_lo + s * 32);
+                            dbh = umma_desc_sw128(b_raw + s * 32);
+                            dbl = umma_desc_sw128(b_lo + s * 32);
+                        } else {  // [16-byte chunk][rows][16 B]: K-adjacent core matrices rows*16 B apart
+                            dah = umma_desc(a_raw + s * 2 * TM_M * 16, TM_M * 16, 128);
+                            dal = umma_desc(a_lo + s * 2 * TM_M * 16, TM_M * 16, 128);
+                            dbh = umma_desc(b_raw + s * 2 * BN * 16, BN * 16, 128);
+                            dbl = umma_desc(b_lo + s * 2 * BN * 16, BN * 16, 128);
+                        }
+                        mma_tf32(d, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
+                        if (!(a.trace & 2)) {  // debug bit 1: hi*hi only (timing experiments only)
+                            mma_tf32(d, dah, dbl, idesc, 1u);
+                            mma_tf32(d, dal, dbh, idesc, 1u);
+                        }
+                    }
+                    tc_commit(smem_u32(&empty_bar[stage]));
+                    if (last) tc_commit(smem_u32(&tfull_bar[slot]));
+                    if (n < 32) B2C_TRACE(a.trace, 144 + n);
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+                if (last) {
+                    kin = 0;
+                    ++cidx;
+                } else {
+                    ++kin;
+                }
             }
         }
         if (lane == 0) B2C_TRACE(a.trace, 5);
-    } else {
-        if (lane == 0) {
-            // ------------------------------------------------------------ TMA / bulk loader
-            int pw = 0, ph = 0, pn = 0;  // MODE 0: im2col base of the tile's first pixel
-            if (MODE == 0) {
+    } else if (lane == 0) {
+        // ------------------------------------------------------------ TMA / bulk loader
+        int stage = 0, n = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+            int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
+            if (MODE == 0 || MODE == 3) {
                 uint32_t b, p, oy, ox;
-                g.fPQ.divmod((uint32_t)m0, b, p);
+                g.fPQ.divmod((uint32_t)w.m0, b, p);
                 g.fOW.divmod(p, oy, ox);
                 pw = (int)ox * g.S - g.P;
                 ph = (int)oy * g.S - g.P;
                 pn = (int)b;
             }
             const char* wsrc = reinterpret_cast<const char*>(a.wpk) +
-                               ((size_t)blockIdx.y * a.kblocks + kb_begin) * (size_t)(2 * Cfg::FLT_ROWS * 128);
-            constexpr uint32_t bytes =
-                Cfg::PIX_ROWS * 128 + (MODE != 1 ? 2 * Cfg::FLT_ROWS * 128 : Cfg::FLT_ROWS * 128);
-            for (int it = 0; it < nkb; ++it) {
-                const int stage = it % STAGES;
-                const uint32_t phase = (uint32_t)(it / STAGES) & 1u;
+                               ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + w.kb_begin) * (size_t)Cfg::FLT_STAGE;
+            for (int i = 0; i < w.nkb; ++i, ++n) {
                 mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
                 const uint32_t bar = smem_u32(&raw_full[stage]);
                 const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
-                const int kb = kb_begin + it;
-                mbar_arrive_expect_tx(bar, bytes);
-                if (it < 32) B2C_TRACE(a.trace, 176 + it);
-                if (MODE == 2) {  // 1x1, stride 1, no pad: x is a plain [pixels][C] NHWC matrix
-                    tma_load_2d(sbase + Cfg::PIX_OFF, &tm_pix, bar, kb * TM_BK, m0);
-                    bulk_g2s(sbase + Cfg::FLT_OFF, wsrc + (size_t)it * (2 * Cfg::FLT_ROWS * 128),
-                             2 * Cfg::FLT_ROWS * 128, bar);
-                } else if (MODE == 0) {
-                    uint32_t tap, cb, ky, kx;
-                    a.fCB.divmod((uint32_t)kb, tap, cb);
-                    g.fR.divmod(tap, ky, kx);
-                    tma_load_im2col_4d(sbase + Cfg::PIX_OFF, &tm_pix, bar, (int)cb * TM_BK, pw, ph, pn,
-                                       (uint16_t)kx, (uint16_t)ky);
-                    bulk_g2s(sbase + Cfg::FLT_OFF, wsrc + (size_t)it * (2 * Cfg::FLT_ROWS * 128),
-                             2 * Cfg::FLT_ROWS * 128, bar);
+                const uint32_t pix = sbase + Cfg::PIX_OFF;
+                const int kb = w.kb_begin + i;
+                // MODE 4 boxes are bx*by rows (<= 128): the rest of the tile keeps
+                // stale (finite) data whose output rows the epilogue discards.
+                mbar_arrive_expect_tx(bar, MODE == 4 ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u : Cfg::BYTES);
+                if (n < 32) B2C_TRACE(a.trace, 176 + n);
+                if (MODE == 1) {
+                    tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
+                    tma_load_2d(sbase + Cfg::FLT_OFF, &tm_flt, bar, kb * TM_BK, w.n0);
                 } else {
-                    tma_load_2d(sbase + Cfg::PIX_OFF, &tm_pix, bar, kb * TM_BK, m0);
-                    tma_load_2d(sbase + Cfg::FLT_OFF, &tm_flt, bar, kb * TM_BK, n0);
+                    if (MODE == 2) {
+                        tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
+                    } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
+                        uint32_t ky, kc;
+                        a.fCB.divmod((uint32_t)kb, ky, kc);
+                        tma_load_5d(pix, &tm_pix, bar, (int)kc * TM_BK, w.ox0, w.oy0, (int)ky, w.b);
+                    } else if (MODE == 0) {
+                        uint32_t tap, cb, ky, kx;
+                        a.fCB.divmod((uint32_t)kb, tap, cb);
+                        g.fR.divmod(tap, ky, kx);
+                        tma_load_im2col_4d(pix, &tm_pix, bar, (int)cb * TM_BK, pw, ph, pn, (uint16_t)kx, (uint16_t)ky);
+                    } else {  // MODE 3: 8 taps x 4 channels, one 16-byte-pixel box per tap
+#pragma unroll 1
+                        for (int j = 0; j < TM_TAPS; ++j) {
+                            const int tap = kb * TM_TAPS + j;
+                            uint32_t ky = 0, kx = 0;
+                            int c = 4;  // taps past R*R: channel 4 is out of bounds -> zeros
+                            if (tap < g.RR) {
+                                g.fR.divmod((uint32_t)tap, ky, kx);
+                                c = 0;
+                            }
+                            tma_load_im2col_4d(pix + (uint32_t)(j * Cfg::PIX_ROWS * 16), &tm_pix, bar, c, pw, ph, pn,
+                                               (uint16_t)kx, (uint16_t)ky);
+                        }
+                    }
+                    bulk_g2s(sbase + Cfg::FLT_OFF, wsrc + (size_t)i * Cfg::FLT_STAGE, Cfg::FLT_STAGE, bar);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
         }
-        __syncwarp();
     }
-    if (tid == 0) B2C_TRACE(a.trace, 6);
+    if (tid == 0) B2C_TRACE(a.trace, 2);
     __syncthreads();
-    if (warp == TM_MMA_WARP) {
+    if (warp == Cfg::MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }

@@ -257,6 +257,15 @@ __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __res
                 g.fR.divmod(tap, ky, kx);
                 const int ic = (int)cb * UMMA_BK + kk;
                 if (ic < g.C) v = w[(long long)oc * g.K + ((long long)ic * g.R + ky) * g.R + kx];
+            } else if (kmode == 5) {  // first layers, x-window: K block = (ky, 32-float window chunk)
+                uint32_t ky, kc;
+                fCB.divmod((uint32_t)kb, ky, kc);
+                const int wi = (int)kc * 32 + kk;  // window float = kx * 4 + channel
+                const int kx = wi >> 2, ch = wi & 3;
+                if (kx < g.R && ch < g.C) v = w[(long long)oc * g.K + ((long long)ch * g.R + ky) * g.R + kx];
+            } else if (kmode == 4) {  // first layers: chunk c = tap kb*8 + c, element e = channel
+                const int tap = kb * 8 + c;
+                if (tap < g.RR && e < g.C) v = w[(long long)oc * g.K + (long long)e * g.RR + tap];
             } else {
                 const int k = kb * UMMA_BK + kk;
                 if (k < g.K) v = w[(long long)oc * g.K + k];

@@ -64,7 +64,9 @@ def test_applicability_reasons():
     assert "tile_n" in backend.applies(d, _tune(backend.VAR_UMMA, tile_n=100))
     assert "1024" in backend.applies(d, _tune(backend.VAR_TILED, mnb0=64, mnb1=32))
     assert "output channels" in backend.applies(_desc(oc=2), _tune(backend.VAR_TILED))
-    assert "in_chans % 4" in backend.applies(d, _tune(backend.VAR_UMMA, tile_n=96, tma=1))
+    assert backend.applies(d, _tune(backend.VAR_UMMA, tile_n=96, tma=1)) is None  # first layer: x-window TMA path
+    assert "swap_ab=0" in backend.applies(d, _tune(backend.VAR_UMMA, tile_n=96, tma=1, swap_ab=1))
+    assert "in_chans % 4" in backend.applies(_desc(ic=6), _tune(backend.VAR_UMMA, tile_n=96, tma=1))
     assert backend.applies(_desc(ic=64), _tune(backend.VAR_UMMA, tile_n=96, tma=1)) is None
     fc = _desc(b=5, ic=256, h=6, w=6, oc=4096, ksz=6, stride=1, pad=0, oh=1, ow=1)
     assert backend.applies(fc, _tune(backend.VAR_FC, tile_n=32, swap_ab=1, split_k=4, tma=1)) is None

@@ -50,7 +50,7 @@ for rep in range(2):
     row("tma_issue", 176)
     row("split_raw", 16)
     row("split_done", 48)
-    row("mma_top", 208)
+    print("  drain/epi  " + " ".join(f"{buf[208 + 2 * i] - t0}/{buf[209 + 2 * i] - t0}" for i in range(24) if buf[208 + 2 * i]))
     row("mma_raw", 80)
     row("mma_split", 112)
     row("mma_commit", 144)
