@@ -81,23 +81,29 @@ struct TmaCfg {
     static constexpr int MMA_WARP = 4 + 4 * DG;
     static constexpr int LOAD_WARP = MMA_WARP + 1;
     static constexpr int THREADS = 32 * (LOAD_WARP + 1);
-    static constexpr int A_ROWS = TM_M;
-    static constexpr int B_ROWS = BN;
-    static constexpr int PIX_ROWS = SWAP ? B_ROWS : A_ROWS;
-    static constexpr int FLT_ROWS = SWAP ? A_ROWS : B_ROWS;
-    static constexpr int A_BYTES = 2 * A_ROWS * 128;  // raw + lo
-    static constexpr int B_BYTES = 2 * B_ROWS * 128;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int PIX_OFF = SWAP ? A_BYTES : 0;  // raw part; lo follows at + PIX_ROWS*128
-    static constexpr int FLT_OFF = SWAP ? 0 : A_BYTES;
+    static constexpr int PIX_ROWS = SWAP ? BN : TM_M;
+    static constexpr int FLT_ROWS = SWAP ? TM_M : BN;
+    // The MMA's A operand (M = 128 rows) lives in TMEM: the split warps move
+    // it there as raw + lo from the smem image the TMA (or bulk copy) wrote.
+    // A is pre-split when it is the packed filter tile (SWAP conv modes).
+    static constexpr bool A_PRESPLIT = SWAP && MODE != 1;
+    static constexpr bool B_SPLIT = SWAP || MODE == 1;  // B raw from TMA: lo computed into smem
+    static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
+    static constexpr int B_BYTES = 2 * BN * 128;  // raw + lo
+    static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
+    static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
+    static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
     static constexpr int FLT_STAGE = 2 * FLT_ROWS * 128;  // packed filters per K block (raw | lo)
+    static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
     static constexpr int BUDGET = TM_MAX_SMEM - TM_HDR - 1024;
-    static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
+    static constexpr int SM_STAGES = BUDGET / STAGE_BYTES;
+    static constexpr int TM_STAGES = (512 - ACC_COLS) / 64;  // A raw + lo: 64 TMEM columns per stage
+    static constexpr int STAGES = SM_STAGES < TM_STAGES ? (SM_STAGES < 8 ? SM_STAGES : 8) : (TM_STAGES < 8 ? TM_STAGES : 8);
     static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    static constexpr int TMEM_COLS = 512;
     static constexpr bool SW128 = MODE != 3;
-    static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
+    static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
     static_assert(STAGES >= 2, "need at least two stages");
     static_assert(DRAIN_COLS % 8 == 0, "TMEM drain granularity");
 };
@@ -217,6 +223,41 @@ __device__ __forceinline__ void split_tile(uint32_t raw, int tid) {
         split_tf32(v.w, h, l3);
         sts128(lo + off, l0, l1, l2, l3);
     }
+}
+
+// Move this thread's A row (M row = tid, 128 threads) into TMEM as 32 raw +
+// 32 lo columns: raw from the smem image at `a` (SWIZZLE_128B rows, or the
+// no-swizzle [chunk][128 rows][16 B] image of MODE 3); lo either computed
+// (x - trunc_tf32(x)) or, for pre-split filter tiles, read from a + 16 KB.
+template <bool SW128, bool PRESPLIT>
+__device__ __forceinline__ void a_to_tmem(uint32_t a, int tid, uint32_t tcol) {
+    float v[32], l[32];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t off = SW128 ? (uint32_t)tid * 128u + (uint32_t)((c ^ (tid & 7)) * 16)
+                                   : (uint32_t)(c * TM_M * 16 + tid * 16);
+        const float4 q = lds128(a + off);
+        v[4 * c] = q.x;
+        v[4 * c + 1] = q.y;
+        v[4 * c + 2] = q.z;
+        v[4 * c + 3] = q.w;
+        if (PRESPLIT) {
+            const float4 r = lds128(a + TM_M * 128 + off);
+            l[4 * c] = r.x;
+            l[4 * c + 1] = r.y;
+            l[4 * c + 2] = r.z;
+            l[4 * c + 3] = r.w;
+        }
+    }
+    if (!PRESPLIT) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float h;
+            split_tf32(v[j], h, l[j]);
+        }
+    }
+    tmem_st32(tcol, v);
+    tmem_st32(tcol + 32, l);
 }
 
 // One unit's output: + bias, ReLU (variants.py:160-165), NCHW stores; with
@@ -370,20 +411,22 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
     pdl_wait();
 
     if (warp < 4) {
-        // ------------------------------------------------------------ split
+        // ------------------------------------------------------------ split: A -> TMEM (raw | lo), B lo -> smem
         int stage = 0, n = 0;
         uint32_t phase = 0;
+        const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);  // this warp's 32 TMEM lanes
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
             const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
             for (int i = 0; i < w.nkb; ++i, ++n) {
                 const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
                 mbar_wait(smem_u32(&raw_full[stage]), phase);
                 if (tid == 0 && n < 32) B2C_TRACE(a.trace, 16 + n);
-                if (!(a.trace & 4)) {  // debug bit 2: skip the split (timing experiments only)
-                    split_tile<Cfg::PIX_ROWS>(sbase + Cfg::PIX_OFF, tid);
-                    if (MODE == 1) split_tile<Cfg::FLT_ROWS>(sbase + Cfg::FLT_OFF, tid);
-                }
+                const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + stage * 64);
+                a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);
+                if (Cfg::B_SPLIT && !(a.trace & 4)) split_tile<BN>(sbase + Cfg::A_SMEM, tid);
                 fence_proxy_async_smem();
+                tmem_st_wait();
+                tc_fence_before();
                 mbar_arrive(smem_u32(&split_full[stage]));
                 if (++stage == STAGES) {
                     stage = 0;
@@ -445,29 +488,25 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
                 tc_fence_after();
                 if (lane == 0 && n < 32) B2C_TRACE(a.trace, 112 + n);
                 if (elect_one_sync()) {
-                    const uint32_t a_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
-                    const uint32_t a_lo = a_raw + TM_M * 128;
-                    const uint32_t b_raw = a_raw + Cfg::A_BYTES;
+                    const uint32_t a_hi = tmem_base + (uint32_t)(Cfg::ACC_COLS + stage * 64);
+                    const uint32_t a_lo = a_hi + 32;
+                    const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
                     const uint32_t b_lo = b_raw + BN * 128;
                     const uint32_t d = tmem_base + (uint32_t)(slot * BN);
 #pragma unroll
                     for (int s = 0; s < TM_BK / 8; ++s) {
-                        uint64_t dah, dal, dbh, dbl;
+                        uint64_t dbh, dbl;
                         if (Cfg::SW128) {
-                            dah = umma_desc_sw128(a_raw + s * 32);
-                            dal = umma_desc_sw128(a_lo + s * 32);
                             dbh = umma_desc_sw128(b_raw + s * 32);
                             dbl = umma_desc_sw128(b_lo + s * 32);
                         } else {  // [16-byte chunk][rows][16 B]: K-adjacent core matrices rows*16 B apart
-                            dah = umma_desc(a_raw + s * 2 * TM_M * 16, TM_M * 16, 128);
-                            dal = umma_desc(a_lo + s * 2 * TM_M * 16, TM_M * 16, 128);
                             dbh = umma_desc(b_raw + s * 2 * BN * 16, BN * 16, 128);
                             dbl = umma_desc(b_lo + s * 2 * BN * 16, BN * 16, 128);
                         }
-                        mma_tf32(d, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
+                        mma_tf32_ts(d, a_hi + 8 * s, dbh, idesc, (first && s == 0) ? 0u : 1u);
                         if (!(a.trace & 2)) {  // debug bit 1: hi*hi only (timing experiments only)
-                            mma_tf32(d, dah, dbl, idesc, 1u);
-                            mma_tf32(d, dal, dbh, idesc, 1u);
+                            mma_tf32_ts(d, a_hi + 8 * s, dbl, idesc, 1u);
+                            mma_tf32_ts(d, a_lo + 8 * s, dbh, idesc, 1u);
                         }
                     }
                     tc_commit(smem_u32(&empty_bar[stage]));

@@ -1,0 +1,13 @@
+OUT=gpurun_out/p7
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu.log 2>&1; tail -2 $OUT/pytest_gpu.log; grep -E "^E .*Assert|Error" $OUT/pytest_gpu.log | head -3
+P="MNt=4:4,MNb=16:16,Kb=4,vw=4,lf=1,li=1"
+for spec in "42 20 BN=128,sk=1,sw=0,dr=0,tm=1" "25 20 BN=32,sk=4,sw=1,dr=0,tm=1" "37 20 BN=96,sk=2,sw=1,dr=0,tm=1" "34 20 BN=96,sk=1,sw=0,dr=0,tm=1"; do set -- $spec
+  timeout 60 python tools/stress_op.py --row $1 --batch $2 --params "$P,$3" --flush --iters 20 >> $OUT/stress.log 2>&1 || echo "exit $? $spec" >> $OUT/stress.log
+done
+timeout 60 python tools/stress_op.py --row 25 --batch 20 --variant conv_fc --params "$P,BN=32,sk=4,sw=1,dr=0,tm=1" --flush --iters 20 >> $OUT/stress.log 2>&1 || echo "exit fc" >> $OUT/stress.log
+for spec in "42 20 BN=128,sk=1,sw=0,dr=0,tm=1" "34 20 BN=96,sk=1,sw=0,dr=0,tm=1" "35 20 BN=64,sk=1,sw=0,dr=0,tm=1" "41 20 BN=192,sk=1,sw=0,dr=0,tm=1" "40 20 BN=96,sk=1,sw=0,dr=0,tm=1" "20 20 BN=96,sk=1,sw=0,dr=0,tm=1" "6 20 BN=64,sk=1,sw=0,dr=0,tm=1" "17 1 BN=32,sk=4,sw=0,dr=0,tm=1" "6 1 BN=32,sk=1,sw=0,dr=0,tm=1" "40 5 BN=96,sk=4,sw=0,dr=0,tm=1"; do set -- $spec
+  timeout 120 python tools/op_overhead.py --row $1 --batch $2 --params "$P,$3" --flags 0 >> $OUT/ovh.log 2>&1
+done
+timeout 120 python tools/trace_op.py --row 42 --batch 20 --params "$P,BN=128,sk=1,sw=0,dr=0,tm=1" --flags 1 2>&1 | grep -v "rep0" > $OUT/trace.log

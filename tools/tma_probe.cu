@@ -25,7 +25,7 @@ constexpr int STAGES = 6;
 
 // mode 0: 2-D boxes (bw cols x bh rows); mode 1: bulk copies of bw*bh*4 bytes
 __global__ void probe(const __grid_constant__ CUtensorMap tm, const float* base, int mode, int bw, int bh,
-                      int cols, int iters, long long* cycles) {
+                      int cols, int iters, int wrap_tiles, long long* cycles) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     const uint32_t tiles = (smem_u32(smem) + 1024 + 1023) & ~1023u;
@@ -44,7 +44,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, const float* base,
             const int s = it % STAGES;
             const uint32_t bar = smem_u32(&bars[s]);
             expect_tx(bar, bytes);
-            const int t = blockIdx.x * iters + it;  // this CTA's t-th tile
+            const int t = (blockIdx.x * iters + it) % wrap_tiles;  // this CTA's t-th tile (wraps: L2-resident runs)
             if (mode == 0) {
                 tma2d(tiles + s * bytes, &tm, bar, (t % tiles_x) * bw, (t / tiles_x) * bh);
             } else {
@@ -94,17 +94,21 @@ int main() {
         }
         const int bytes = c.bw * c.bh * 4;
         const int smem = 2048 + STAGES * bytes;
+        for (int l2 = 0; l2 < 2; ++l2)
         for (int grid : {1, 16, 148}) {
             const long long total_tiles = (long long)rows * cols * 4 / bytes;
             int iters = (int)std::min<long long>(total_tiles / grid, 2048);
-            for (int rep = 0; rep < 2; ++rep) probe<<<grid, 32, smem>>>(tm, d, c.mode, c.bw, c.bh, cols, iters, cyc);
+            // l2: re-read a 32 MB window (L2-resident after the first pass)
+            const int wrap = l2 ? (int)((32ll << 20) / bytes) : (int)total_tiles;
+            if (l2) iters = 512;
+            for (int rep = 0; rep < 2; ++rep) probe<<<grid, 32, smem>>>(tm, d, c.mode, c.bw, c.bh, cols, iters, wrap, cyc);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
             std::vector<long long> h(grid);
             cudaMemcpy(h.data(), cyc, grid * 8, cudaMemcpyDeviceToHost);
             long long mx = 0;
             for (auto v : h) mx = v > mx ? v : mx;
-            printf("%-34s grid %3d: %6.1f B/clk/SM  (%d tiles/CTA, %lld cyc)\n", c.name, grid,
+            printf("%-34s %s grid %3d: %6.1f B/clk/SM  (%d tiles/CTA, %lld cyc)\n", c.name, l2 ? "L2  " : "DRAM", grid,
                    (double)iters * bytes / mx, iters, mx);
         }
     }
