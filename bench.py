@@ -58,6 +58,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--debug-flags", type=int, default=0,
+                    help="library debug flags (measurement experiments only; results are then not valid bench lines)")
     return ap.parse_args()
 
 
@@ -209,6 +211,9 @@ def run_ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    if args.debug_flags:
+        from paper_1611_06945_b200 import backend as _bk
+        _bk.lib().b2c_debug_trace_enable(args.debug_flags & ~1)  # never the (CTA-0 trace) bit
     batches = [int(b) for b in args.batches.split(",")]
     db_path = args.db or tuner.shipped_db_path()
     db = tuner.load_db(db_path) if (os.path.exists(db_path) and not args.heuristic) else None

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -175,10 +176,12 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
 struct UmmaPlan {
     int grid_x, grid_y, split, kps, kblocks, cblocks, tiles, kmode, flt_rows, tma;
     int bx, by, tiles_x, tiles_y, hp, wp;  // kmode 5: pixel blocks and the padded NHWC extent
+    int parts;                             // packed filter halves per K block (2: raw | lo, 1: raw)
     size_t wpk_bytes;   // packed filters (offset 0 of the workspace; 0 for the TMA fc path)
     size_t part_off;    // split-K partials
     size_t sems_off;    // split-K tickets
     size_t nhwc_off;    // TMA conv path: NHWC copy of x
+    size_t gbar_off;    // TMA path: grid-barrier counter
     size_t ws_bytes;    // total
 };
 
@@ -211,7 +214,9 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     const int want = std::max(1, std::min(t->split_k, p.kblocks));
     p.kps = (p.kblocks + want - 1) / want;
     p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
-    p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * 2 * p.flt_rows * UMMA_BK * sizeof(float);
+    // packed filters: raw | lo per K block; raw only when the TMA kernel takes them as its TMEM A operand
+    p.parts = (p.tma && t->swap_ab) ? 1 : 2;
+    p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * p.parts * p.flt_rows * UMMA_BK * sizeof(float);
     p.part_off = align256(p.wpk_bytes);
     p.sems_off = p.part_off;
     if (p.split > 1) p.sems_off += align256((size_t)p.tiles * p.split * BN * UMMA_M * sizeof(float));
@@ -219,7 +224,8 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     const bool nhwc = p.tma && (p.kmode == 3 || p.kmode == 4 || p.kmode == 5);
     const int cp = p.kmode >= 4 ? 4 : d->c;  // first layers: channels padded to 4 (16-byte pixels)
     const size_t pix = p.kmode == 5 ? (size_t)p.hp * p.wp : (size_t)d->h * d->w;
-    p.ws_bytes = p.nhwc_off + (nhwc ? align256((size_t)d->n * cp * pix * sizeof(float)) : 0);
+    p.gbar_off = p.nhwc_off + (nhwc ? align256((size_t)d->n * cp * pix * sizeof(float)) : 0);
+    p.ws_bytes = p.gbar_off + (p.tma ? 256 : 0);  // grid-barrier counter of the fused re-layout
     return p;
 }
 
@@ -271,7 +277,8 @@ int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* w
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
     k_pack_filters<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<float*>(ws), p.flt_rows, p.kblocks,
                                            FastDiv((uint32_t)p.cblocks), p.kmode, total,
-                                           (p.tma && (p.kmode == 3 || p.kmode == 5)) ? 1 : 0);  // SWIZZLE_128B image
+                                           (p.tma && (p.kmode == 3 || p.kmode == 5)) ? 1 : 0,  // SWIZZLE_128B image
+                                           p.parts);
     return B2C_OK;
 }
 
@@ -405,7 +412,8 @@ cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool no_pdl = std::getenv("B2C_NO_PDL") != nullptr;  // A/B switch for measurements
+    cfg.numAttrs = no_pdl ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
 }
 
@@ -476,11 +484,16 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     char* wsb = reinterpret_cast<char*>(ws);
     CUtensorMap tm_pix, tm_flt;
     std::memset(&tm_flt, 0, sizeof(tm_flt));
+    // x re-layout: a separate PDL-launched kernel (default; measured faster) or,
+    // with B2C_FUSED_NHWC set, inside k_tconv before a grid barrier.
+    static const bool separate = std::getenv("B2C_FUSED_NHWC") == nullptr;
+    int relayout = 0;
     if (mode == 4) {
         float* xp = reinterpret_cast<float*>(wsb + p.nhwc_off);
         const long long total = (long long)d->n * p.hp * p.wp;
         const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
-        if (!(g_trace_on & 16)) {
+        if (!separate) relayout = 2;
+        else if (!(g_trace_on & 16)) {
             cudaError_t le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, x, reinterpret_cast<float4*>(xp),
                                         (int)d->c, (int)d->h, (int)d->w, p.hp, p.wp, (int)d->pad, total);
             if (le != cudaSuccess) return cuda_fail(le, "k_to_nhwc4_pad launch");
@@ -491,7 +504,8 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         float* xh = reinterpret_cast<float*>(wsb + p.nhwc_off);
         const int HW = d->h * d->w;
         const int cp = mode == 3 ? 4 : d->c;
-        if (!(g_trace_on & 16)) {  // debug bit 4: reuse the NHWC copy already in the workspace
+        if (!separate && mode != 3) relayout = 1;
+        else if (!(g_trace_on & 16)) {  // debug bit 4: reuse the NHWC copy already in the workspace
             cudaError_t le;
             if (mode == 3) {
                 const long long total = (long long)d->n * HW;
@@ -534,6 +548,13 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.ws = reinterpret_cast<float*>(wsb + p.part_off);
     a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
     a.trace = g_trace_on & 15;
+    a.relayout = (g_trace_on & 16) ? 0 : relayout;
+    a.x = x;
+    a.xh = reinterpret_cast<float*>(wsb + p.nhwc_off);
+    a.hp = p.hp;
+    a.wp = p.wp;
+    a.pad = d->pad;
+    a.gbar = reinterpret_cast<unsigned long long*>(wsb + p.gbar_off);
     const int grid = std::min(a.units, num_sms());
     cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, tm_pix, tm_flt, a);
     if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
@@ -764,7 +785,8 @@ int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
     (void)d;
     if (!t) return 0;
     const int pack = (is_umma(t->variant) && !t->prepared && !(t->tma && t->variant == B2C_VAR_FC)) ? 1 : 0;
-    const int nhwc = (is_umma(t->variant) && t->tma && t->variant != B2C_VAR_FC) ? 1 : 0;
+    const bool sep = std::getenv("B2C_FUSED_NHWC") == nullptr || (t->tma == 2 && d && d->c <= 4);
+    const int nhwc = (is_umma(t->variant) && t->tma && t->variant != B2C_VAR_FC && sep) ? 1 : 0;
     return 1 + pack + nhwc;
 }
 

@@ -85,15 +85,15 @@ struct TmaCfg {
     static constexpr int FLT_ROWS = SWAP ? TM_M : BN;
     // The MMA's A operand (M = 128 rows) lives in TMEM: the split warps move
     // it there as raw + lo from the smem image the TMA (or bulk copy) wrote.
-    // A is pre-split when it is the packed filter tile (SWAP conv modes).
-    static constexpr bool A_PRESPLIT = SWAP && MODE != 1;
+    // lo is computed on the way (filters, when they are A, are packed raw-only).
+    static constexpr bool A_PRESPLIT = false;
     static constexpr bool B_SPLIT = SWAP || MODE == 1;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
     static constexpr int B_BYTES = 2 * BN * 128;  // raw + lo
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
     static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
-    static constexpr int FLT_STAGE = 2 * FLT_ROWS * 128;  // packed filters per K block (raw | lo)
+    static constexpr int FLT_STAGE = (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block (raw [| lo])
     static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
     static constexpr int BUDGET = TM_MAX_SMEM - TM_HDR - 1024;
     static constexpr int SM_STAGES = BUDGET / STAGE_BYTES;
@@ -123,6 +123,14 @@ struct TArgs {
     FastDiv fCB;        // MODE 0: channel blocks of 32 per filter tap
     int drain;
     int trace;          // debug: phase clocks of CTA 0 into g_b2c_trace
+    // In-kernel re-layout of x (instead of a separate conversion launch):
+    // 0 none (x already converted / fc), 1 NCHW -> NHWC (C channels),
+    // 2 NCHW -> zero-padded NHWC4 [N][hp][wp][4] (first layers).
+    int relayout;
+    const float* x;
+    float* xh;
+    int hp, wp, pad;
+    unsigned long long* gbar;  // grid barrier counter (monotonic; zero at allocation)
 };
 
 struct Unit {
@@ -202,6 +210,77 @@ __global__ void __launch_bounds__(256) k_to_nhwc4_pad(const float* __restrict__ 
         }
         xp[i] = make_float4(v[0], v[1], v[2], v[3]);
     }
+}
+
+// ----------------------------------------------------------------------------- fused re-layout
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Every CTA converts its share of x into the workspace copy the TMA reads,
+// then all CTAs meet at a grid barrier (grid <= #SMs with one CTA per SM, so
+// all CTAs are co-resident).  Saves a kernel boundary per op.  `scratch` is
+// the (still unused) pipeline smem: a 32 x 33 transpose tile per warp.
+__device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
+    const Geom& g = a.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    if (a.relayout == 1) {
+        float* tile = reinterpret_cast<float*>(scratch) + warp * (32 * 33);
+        const int tp = (g.HW + 31) / 32, tc = (g.C + 31) / 32;
+        const long long ntiles = (long long)g.N * tp * tc;
+        for (long long t = (long long)blockIdx.x * nwarps + warp; t < ntiles; t += (long long)gridDim.x * nwarps) {
+            const int ci = (int)(t % tc);
+            const long long r = t / tc;
+            const int pi = (int)(r % tp), n = (int)(r / tp);
+            const int p0 = pi * 32, c0 = ci * 32;
+            const float* src = a.x + (size_t)n * g.C * g.HW;
+            float* dst = a.xh + (size_t)n * g.HW * g.C;
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const int c = c0 + j, p = p0 + lane;
+                tile[j * 33 + lane] = (c < g.C && p < g.HW) ? __ldg(src + (size_t)c * g.HW + p) : 0.0f;
+            }
+            __syncwarp();
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const int p = p0 + j, c = c0 + lane;
+                if (p < g.HW && c < g.C) dst[(size_t)p * g.C + c] = tile[lane * 33 + j];
+            }
+            __syncwarp();
+        }
+    } else if (a.relayout == 2) {
+        const long long total = (long long)g.N * a.hp * a.wp;
+        float4* dst = reinterpret_cast<float4*>(a.xh);
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+             i += (long long)gridDim.x * blockDim.x) {
+            const int xq = (int)(i % a.wp);
+            const long long t = i / a.wp;
+            const int yq = (int)(t % a.hp), b = (int)(t / a.hp);
+            const int iy = yq - a.pad, ix = xq - a.pad;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if ((unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W) {
+                const float* src = a.x + ((size_t)b * g.C * g.H + iy) * g.W + ix;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < g.C) v[c] = __ldg(src + (size_t)c * g.HW);
+            }
+            dst[i] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+    }
+    // publish (generic-proxy writes -> other CTAs' TMA reads) and meet
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long ticket = atomicAdd(a.gbar, 1ull);
+        const unsigned long long target = (ticket / gridDim.x + 1ull) * gridDim.x;
+        while (ld_acquire_u64(a.gbar) < target) __nanosleep(64);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
 }
 
 // ----------------------------------------------------------------------------- split + epilogue helpers
@@ -409,6 +488,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
     if (tid == 0) B2C_TRACE(a.trace, 1);
     pdl_launch_dependents();
     pdl_wait();
+    if (a.relayout) fused_relayout(a, smem + TM_HDR + 1024);
+    if (tid == 0) B2C_TRACE(a.trace, 3);
 
     if (warp < 4) {
         // ------------------------------------------------------------ split: A -> TMEM (raw | lo), B lo -> smem

@@ -232,9 +232,11 @@ __device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* acc) {
 //   part 0: W[oc][k], part 1: W - trunc_tf32(W), oc = t*ROWS + r, k = k-index(kb, 4c+e)
 // swz != 0 writes each (tile, K block, part) as 128-byte rows with 16-byte
 // chunks XOR-swizzled by row % 8 (the SWIZZLE_128B image k_tconv reads).
+// parts == 1 packs the raw half only (k_tconv computes lo itself when the
+// filter tile is its TMEM A operand).
 __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __restrict__ w, float* __restrict__ out,
                                                       int rows, int kblocks, FastDiv fCB, int kmode,
-                                                      long long total, int swz) {
+                                                      long long total, int swz, int parts) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const int e = (int)(i & 3);
@@ -243,8 +245,8 @@ __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __res
         t /= rows;
         const int c = (int)(t & 7);
         t >>= 3;
-        const int part = (int)(t & 1);
-        t >>= 1;
+        const int part = parts == 2 ? (int)(t & 1) : 0;  // parts == 1: raw only
+        if (parts == 2) t >>= 1;
         const int kb = (int)(t % kblocks);
         const int tile = (int)(t / kblocks);
         const int oc = tile * rows + r;
