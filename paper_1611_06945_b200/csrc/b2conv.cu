@@ -154,6 +154,7 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
     if (t->tma < 0 || t->tma > 2) { why = "tma must be 0, 1 or 2"; return B2C_BAD_ARGS; }
+    if (t->tma && t->stages == 2 && t->tile_n > 64) { why = "two CTAs per SM (stages=2) need tile_n <= 64"; return B2C_INAPPLICABLE; }
     if (t->tma == 2 && !(d->r == 1 && d->stride == 1 && d->pad == 0) && t->variant != B2C_VAR_FC && d->c > 4) {
         why = "tma=2 (2-D tiled pixels) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
     }
@@ -425,36 +426,43 @@ struct TconvEntry {
     int threads;
 };
 
-template <int BN, bool SWAP, int MODE>
+template <int BN, bool SWAP, int MODE, int OCC>
 TconvEntry tconv_entry() {
-    using C = TmaCfg<BN, SWAP, MODE>;
-    return TconvEntry{&k_tconv<BN, SWAP, MODE>, C::SMEM, C::THREADS};
+    using C = TmaCfg<BN, SWAP, MODE, OCC>;
+    return TconvEntry{&k_tconv<BN, SWAP, MODE, OCC>, C::SMEM, C::THREADS};
 }
 
 template <bool SWAP, int MODE>
-TconvEntry tconv_pick_bn(int bn) {
+TconvEntry tconv_pick_bn(int bn, int occ) {
+    if (occ == 2) {
+        switch (bn) {
+            case 32: return tconv_entry<32, SWAP, MODE, 2>();
+            case 64: return tconv_entry<64, SWAP, MODE, 2>();
+        }
+        return TconvEntry{nullptr, 0, 0};
+    }
     switch (bn) {
-        case 32: return tconv_entry<32, SWAP, MODE>();
-        case 64: return tconv_entry<64, SWAP, MODE>();
-        case 96: return tconv_entry<96, SWAP, MODE>();
-        case 128: return tconv_entry<128, SWAP, MODE>();
-        case 192: return tconv_entry<192, SWAP, MODE>();
+        case 32: return tconv_entry<32, SWAP, MODE, 1>();
+        case 64: return tconv_entry<64, SWAP, MODE, 1>();
+        case 96: return tconv_entry<96, SWAP, MODE, 1>();
+        case 128: return tconv_entry<128, SWAP, MODE, 1>();
+        case 192: return tconv_entry<192, SWAP, MODE, 1>();
     }
     return TconvEntry{nullptr, 0, 0};
 }
 
 template <int MODE>
-TconvEntry tconv_pick_sw(int bn, int swap) {
-    return swap ? tconv_pick_bn<true, MODE>(bn) : tconv_pick_bn<false, MODE>(bn);
+TconvEntry tconv_pick_sw(int bn, int swap, int occ) {
+    return swap ? tconv_pick_bn<true, MODE>(bn, occ) : tconv_pick_bn<false, MODE>(bn, occ);
 }
 
-TconvEntry tconv_pick(int bn, int swap, int mode) {
+TconvEntry tconv_pick(int bn, int swap, int mode, int occ) {
     switch (mode) {
-        case 0: return tconv_pick_sw<0>(bn, swap);
-        case 1: return tconv_pick_sw<1>(bn, swap);
-        case 2: return tconv_pick_sw<2>(bn, swap);
-        case 3: return tconv_pick_sw<3>(bn, swap);
-        case 4: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 4>(bn);
+        case 0: return tconv_pick_sw<0>(bn, swap, occ);
+        case 1: return tconv_pick_sw<1>(bn, swap, occ);
+        case 2: return tconv_pick_sw<2>(bn, swap, occ);
+        case 3: return tconv_pick_sw<3>(bn, swap, occ);
+        case 4: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 4>(bn, occ);
     }
     return TconvEntry{nullptr, 0, 0};
 }
@@ -476,7 +484,8 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     if (rc) return rc;
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
     const int mode = p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
-    TconvEntry e = tconv_pick(t->tile_n, t->swap_ab, mode);
+    const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
+    TconvEntry e = tconv_pick(t->tile_n, t->swap_ab, mode, occ);
     if (!e.fn) return fail(B2C_INAPPLICABLE, "no TMA tcgen05 kernel for this tile");
     rc = ensure_smem_attr((const void*)e.fn, e.smem);
     if (rc) return rc;
@@ -555,7 +564,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.wp = p.wp;
     a.pad = d->pad;
     a.gbar = reinterpret_cast<unsigned long long*>(wsb + p.gbar_off);
-    const int grid = std::min(a.units, num_sms());
+    const int grid = std::min(a.units, occ * num_sms());
     cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, tm_pix, tm_flt, a);
     if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
     return B2C_OK;

@@ -72,10 +72,12 @@ constexpr int TM_HDR = 2048;           // barriers, TMEM slot, flags (< 1 KB); u
 constexpr int TM_MAX_SMEM = 232448;    // 227 KB opt-in per CTA
 constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 
-template <int BN, bool SWAP, int MODE>
+template <int BN, bool SWAP, int MODE, int OCC = 1>
 struct TmaCfg {
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
-    static constexpr int DG = BN > 128 ? 2 : 1;  // drain warp groups (column halves)
+    static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
+    // drain warp groups (column halves); two groups halve the exposed epilogue
+    static constexpr int DG = (OCC == 1 && (BN >= 64 || SWAP)) ? 2 : 1;
     static constexpr int DRAIN_COLS = BN / DG;
     static constexpr int DRAIN_THREADS = 128 * DG;
     static constexpr int MMA_WARP = 4 + 4 * DG;
@@ -95,12 +97,14 @@ struct TmaCfg {
     static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
     static constexpr int FLT_STAGE = (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block (raw [| lo])
     static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
-    static constexpr int BUDGET = TM_MAX_SMEM - TM_HDR - 1024;
+    // OCC CTAs per SM share its 228 KB of shared memory (1 KB per CTA is the driver's) and 512 TMEM columns
+    static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024;
     static constexpr int SM_STAGES = BUDGET / STAGE_BYTES;
-    static constexpr int TM_STAGES = (512 - ACC_COLS) / 64;  // A raw + lo: 64 TMEM columns per stage
-    static constexpr int STAGES = SM_STAGES < TM_STAGES ? (SM_STAGES < 8 ? SM_STAGES : 8) : (TM_STAGES < 8 ? TM_STAGES : 8);
+    static constexpr int STAGES = SM_STAGES < 8 ? SM_STAGES : 8;
     static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES;
-    static constexpr int TMEM_COLS = 512;
+    static constexpr int A_SLOTS = 2;                        // TMEM A stages (raw | lo: 64 columns each)
+    static constexpr int TMEM_COLS = OCC == 2 ? 256 : 512;
+    static_assert(ACC_COLS + A_SLOTS * 64 <= TMEM_COLS, "TMEM budget");
     static constexpr bool SW128 = MODE != 3;
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
     static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
@@ -441,10 +445,10 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
 
 // ----------------------------------------------------------------------------- main kernel
 
-template <int BN, bool SWAP, int MODE>
-__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
+template <int BN, bool SWAP, int MODE, int OCC>
+__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
     k_tconv(const __grid_constant__ CUtensorMap tm_pix, const __grid_constant__ CUtensorMap tm_flt, TArgs a) {
-    using Cfg = TmaCfg<BN, SWAP, MODE>;
+    using Cfg = TmaCfg<BN, SWAP, MODE, OCC>;
     constexpr int STAGES = Cfg::STAGES;
     constexpr int DC = Cfg::DRAIN_COLS;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
     uint64_t* empty_bar = split_full + STAGES;
     uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
     uint64_t* tempty_bar = tfull_bar + 2;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* afree_bar = tempty_bar + 2;      // [A_SLOTS] TMEM A slot consumed by the MMAs
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afree_bar + Cfg::A_SLOTS);
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* bias_s = reinterpret_cast<float*>(smem + 1024);
     const uint32_t tiles_u32 = (smem_u32(smem) + TM_HDR + 1023u) & ~1023u;
@@ -474,6 +479,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
             mbar_init(smem_u32(&tfull_bar[s]), 1);
             mbar_init(smem_u32(&tempty_bar[s]), Cfg::DRAIN_THREADS);
         }
+        for (int s = 0; s < Cfg::A_SLOTS; ++s) mbar_init(smem_u32(&afree_bar[s]), 1);
         mbar_fence_init();
     }
     if (warp == Cfg::MMA_WARP) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
@@ -502,7 +508,11 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
                 const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
                 mbar_wait(smem_u32(&raw_full[stage]), phase);
                 if (tid == 0 && n < 32) B2C_TRACE(a.trace, 16 + n);
-                const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + stage * 64);
+                const int aslot = n % Cfg::A_SLOTS;
+                if (n >= Cfg::A_SLOTS)  // the MMAs of iteration n - A_SLOTS are done with this TMEM slot
+                    mbar_wait(smem_u32(&afree_bar[aslot]), (uint32_t)((n / Cfg::A_SLOTS) - 1) & 1u);
+                tc_fence_after();
+                const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + aslot * 64);
                 a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);
                 if (Cfg::B_SPLIT && !(a.trace & 4)) split_tile<BN>(sbase + Cfg::A_SMEM, tid);
                 fence_proxy_async_smem();
@@ -569,7 +579,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
                 tc_fence_after();
                 if (lane == 0 && n < 32) B2C_TRACE(a.trace, 112 + n);
                 if (elect_one_sync()) {
-                    const uint32_t a_hi = tmem_base + (uint32_t)(Cfg::ACC_COLS + stage * 64);
+                    const uint32_t a_hi = tmem_base + (uint32_t)(Cfg::ACC_COLS + (n % Cfg::A_SLOTS) * 64);
                     const uint32_t a_lo = a_hi + 32;
                     const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
                     const uint32_t b_lo = b_raw + BN * 128;
@@ -591,6 +601,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE>::THREADS, 1)
                         }
                     }
                     tc_commit(smem_u32(&empty_bar[stage]));
+                    tc_commit(smem_u32(&afree_bar[n % Cfg::A_SLOTS]));
                     if (last) tc_commit(smem_u32(&tfull_bar[slot]));
                     if (n < 32) B2C_TRACE(a.trace, 144 + n);
                 }
