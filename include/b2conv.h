@@ -81,7 +81,8 @@ typedef struct b2c_conv_desc {
 /* Variant + tuning knobs, the C form of TuneParams (variants.py:39-91).
  * FFMA variants read mnt/mnb/kb/vw with the reference's meaning (register
  * block, thread block, k unroll, vector width).  The tcgen05 variants read
- * tile_n (MMA N), stages (< 0 disables the cooperative L2 prefetch of x/w
+ * tile_n (MMA N), stages (TMA kernel: CTAs per SM, 1 or 2 [2 needs tile_n <= 64];
+ * gather kernel: < 0 disables the cooperative L2 prefetch of x/w
  * that small ops get by default), split_k, swap_ab (0: M = output pixels, N =
  * out_chans; 1: M = out_chans, N = output pixels) and drain (K blocks of 32
  * accumulated in one TMEM chunk before it is drained into fp32 registers;
@@ -95,8 +96,10 @@ typedef struct b2c_tune {
     int32_t mnt0, mnt1, mnb0, mnb1, kb, vw;
     int32_t tile_n, stages, split_k, swap_ab, drain, prepared;
     int32_t tma; /* tcgen05 variants: 0 = operands gathered by producer warps from NCHW (k_umma);
-                    1 = TMA-fed (k_tconv): im2col TMA on an NHWC copy of x made in the workspace
-                    by the same call, or 2-D TMA of raw x / w for conv_fc */
+                    1 = TMA-fed persistent kernel (k_tconv): im2col TMA on an NHWC copy of x made
+                    in the workspace by the same call (first layers, C <= 4: x-window boxes on a
+                    padded NHWC4 copy), or 2-D TMA of raw x / w for conv_fc;
+                    2 = as 1, but 2-D tiles for 1x1/stride-1 convs and 8-tap 16-byte boxes for C <= 4 */
 } b2c_tune;
 
 /* 0 when `tune` can run `d`; otherwise B2C_INAPPLICABLE / B2C_BAD_ARGS with a
