@@ -100,6 +100,9 @@ typedef struct b2c_tune {
                     in the workspace by the same call (first layers, C <= 4: x-window boxes on a
                     padded NHWC4 copy), or 2-D TMA of raw x / w for conv_fc;
                     2 = as 1, but 2-D tiles for 1x1/stride-1 convs and 8-tap 16-byte boxes for C <= 4 */
+    int32_t cluster; /* TMA kernel: 2 = CTA pairs (thread-block clusters) take neighbouring pixel tiles of the
+                        same filter tile and multicast each filter stage to both (half the filter L2 traffic);
+                        0/1 = single CTAs.  Pairs need swap_ab = 0 and a conv (not fc) variant. */
 } b2c_tune;
 
 /* 0 when `tune` can run `d`; otherwise B2C_INAPPLICABLE / B2C_BAD_ARGS with a
@@ -111,7 +114,9 @@ int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, si
  * shared-memory image [raw | lo = w - trunc_tf32(w)].  No-op (B2C_OK) for the
  * FFMA variants.  This is the B200 form of ConvTiled.required_formats
  * (variants.py:416-424: K-major padded filters) + the conversion execute_node
- * applies (runner.py:96-98), done once per filter tensor instead of per call. */
+ * applies (runner.py:96-98), done once per filter tensor instead of per call.
+ * Synchronises `stream` before returning (a one-time setup call), so that
+ * launches with prepared != 0 may read the pack without stream ordering. */
 int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* workspace,
                      size_t ws_bytes, void* stream);
 

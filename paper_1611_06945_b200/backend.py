@@ -50,7 +50,7 @@ class ConvDesc(ctypes.Structure):
 
 class Tune(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
-        "variant", "mnt0", "mnt1", "mnb0", "mnb1", "kb", "vw", "tile_n", "stages", "split_k", "swap_ab", "drain", "prepared", "tma")]
+        "variant", "mnt0", "mnt1", "mnb0", "mnb1", "kb", "vw", "tile_n", "stages", "split_k", "swap_ab", "drain", "prepared", "tma", "cluster")]
 
 
 _lib = None

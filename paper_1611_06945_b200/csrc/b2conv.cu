@@ -155,6 +155,11 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
     if (t->tma < 0 || t->tma > 2) { why = "tma must be 0, 1 or 2"; return B2C_BAD_ARGS; }
     if (t->tma && t->stages == 2 && t->tile_n > 64) { why = "two CTAs per SM (stages=2) need tile_n <= 64"; return B2C_INAPPLICABLE; }
+    if (t->cluster == 2 && (!t->tma || t->swap_ab || t->variant == B2C_VAR_FC || t->tile_n < 64 || t->stages == 2)) {
+        why = "CTA pairs (cluster=2) need the TMA kernel, swap_ab=0, a conv variant, tile_n >= 64, 1 CTA/SM";
+        return B2C_INAPPLICABLE;
+    }
+    if (t->cluster == 2 && t->tma == 2 && d->c <= 4) { why = "CTA pairs: not with the 8-tap first-layer path"; return B2C_INAPPLICABLE; }
     if (t->tma == 2 && !(d->r == 1 && d->stride == 1 && d->pad == 0) && t->variant != B2C_VAR_FC && d->c > 4) {
         why = "tma=2 (2-D tiled pixels) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
     }
@@ -403,18 +408,30 @@ int encode_rows(CUtensorMap* tm, const float* base, long long rows, long long co
 }
 
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                       Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
     static const bool no_pdl = std::getenv("B2C_NO_PDL") != nullptr;  // A/B switch for measurements
-    cfg.numAttrs = no_pdl ? 0 : 1;
+    if (!no_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cluster;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
 }
 
@@ -426,43 +443,54 @@ struct TconvEntry {
     int threads;
 };
 
-template <int BN, bool SWAP, int MODE, int OCC>
+template <int BN, bool SWAP, int MODE, int OCC, int CL>
 TconvEntry tconv_entry() {
-    using C = TmaCfg<BN, SWAP, MODE, OCC>;
-    return TconvEntry{&k_tconv<BN, SWAP, MODE, OCC>, C::SMEM, C::THREADS};
+    using C = TmaCfg<BN, SWAP, MODE, OCC, CL>;
+    return TconvEntry{&k_tconv<BN, SWAP, MODE, OCC, CL>, C::SMEM, C::THREADS};
 }
 
 template <bool SWAP, int MODE>
-TconvEntry tconv_pick_bn(int bn, int occ) {
+TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
+    if (cl == 2) {
+        if constexpr (!SWAP && MODE != 1) {
+            switch (bn) {
+                case 64: return tconv_entry<64, false, MODE, 1, 2>();
+                case 96: return tconv_entry<96, false, MODE, 1, 2>();
+                case 128: return tconv_entry<128, false, MODE, 1, 2>();
+                case 192: return tconv_entry<192, false, MODE, 1, 2>();
+            }
+        }
+        return TconvEntry{nullptr, 0, 0};
+    }
     if (occ == 2) {
         switch (bn) {
-            case 32: return tconv_entry<32, SWAP, MODE, 2>();
-            case 64: return tconv_entry<64, SWAP, MODE, 2>();
+            case 32: return tconv_entry<32, SWAP, MODE, 2, 1>();
+            case 64: return tconv_entry<64, SWAP, MODE, 2, 1>();
         }
         return TconvEntry{nullptr, 0, 0};
     }
     switch (bn) {
-        case 32: return tconv_entry<32, SWAP, MODE, 1>();
-        case 64: return tconv_entry<64, SWAP, MODE, 1>();
-        case 96: return tconv_entry<96, SWAP, MODE, 1>();
-        case 128: return tconv_entry<128, SWAP, MODE, 1>();
-        case 192: return tconv_entry<192, SWAP, MODE, 1>();
+        case 32: return tconv_entry<32, SWAP, MODE, 1, 1>();
+        case 64: return tconv_entry<64, SWAP, MODE, 1, 1>();
+        case 96: return tconv_entry<96, SWAP, MODE, 1, 1>();
+        case 128: return tconv_entry<128, SWAP, MODE, 1, 1>();
+        case 192: return tconv_entry<192, SWAP, MODE, 1, 1>();
     }
     return TconvEntry{nullptr, 0, 0};
 }
 
 template <int MODE>
-TconvEntry tconv_pick_sw(int bn, int swap, int occ) {
-    return swap ? tconv_pick_bn<true, MODE>(bn, occ) : tconv_pick_bn<false, MODE>(bn, occ);
+TconvEntry tconv_pick_sw(int bn, int swap, int occ, int cl) {
+    return swap ? tconv_pick_bn<true, MODE>(bn, occ, cl) : tconv_pick_bn<false, MODE>(bn, occ, cl);
 }
 
-TconvEntry tconv_pick(int bn, int swap, int mode, int occ) {
+TconvEntry tconv_pick(int bn, int swap, int mode, int occ, int cl) {
     switch (mode) {
-        case 0: return tconv_pick_sw<0>(bn, swap, occ);
-        case 1: return tconv_pick_sw<1>(bn, swap, occ);
-        case 2: return tconv_pick_sw<2>(bn, swap, occ);
-        case 3: return tconv_pick_sw<3>(bn, swap, occ);
-        case 4: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 4>(bn, occ);
+        case 0: return tconv_pick_sw<0>(bn, swap, occ, cl);
+        case 1: return tconv_pick_sw<1>(bn, swap, occ, cl);
+        case 2: return tconv_pick_sw<2>(bn, swap, occ, cl);
+        case 3: return tconv_pick_sw<3>(bn, swap, occ, cl);
+        case 4: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 4>(bn, occ, cl);
     }
     return TconvEntry{nullptr, 0, 0};
 }
@@ -485,7 +513,8 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
     const int mode = p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
-    TconvEntry e = tconv_pick(t->tile_n, t->swap_ab, mode, occ);
+    const int cl = t->cluster == 2 ? 2 : 1;
+    TconvEntry e = tconv_pick(t->tile_n, t->swap_ab, mode, occ, cl);
     if (!e.fn) return fail(B2C_INAPPLICABLE, "no TMA tcgen05 kernel for this tile");
     rc = ensure_smem_attr((const void*)e.fn, e.smem);
     if (rc) return rc;
@@ -503,7 +532,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
         if (!separate) relayout = 2;
         else if (!(g_trace_on & 16)) {
-            cudaError_t le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, x, reinterpret_cast<float4*>(xp),
+            cudaError_t le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, 1, x, reinterpret_cast<float4*>(xp),
                                         (int)d->c, (int)d->h, (int)d->w, p.hp, p.wp, (int)d->pad, total);
             if (le != cudaSuccess) return cuda_fail(le, "k_to_nhwc4_pad launch");
         }
@@ -519,11 +548,11 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
             if (mode == 3) {
                 const long long total = (long long)d->n * HW;
                 const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
-                le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, x, reinterpret_cast<float4*>(xh),
+                le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, 1, x, reinterpret_cast<float4*>(xh),
                                 (int)d->c, (int)d->h, (int)d->w, (int)d->h, (int)d->w, 0, total);
             } else {
                 dim3 tgrid((HW + 31) / 32, (cp + 31) / 32, d->n);
-                le = launch_pdl(k_nchw_to_nhwc, tgrid, dim3(256), 0, st, x, xh, (int)d->c, cp, HW);
+                le = launch_pdl(k_nchw_to_nhwc, tgrid, dim3(256), 0, st, 1, x, xh, (int)d->c, cp, HW);
             }
             if (le != cudaSuccess) return cuda_fail(le, "NHWC conversion launch");
         }
@@ -547,7 +576,9 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.kps = p.kps;
     a.kblocks = p.kblocks;
     a.tiles_n = p.grid_y;
-    a.units = p.tiles * p.split;
+    a.tiles_m = p.grid_x;
+    // CL = 2: units are pair-units (two neighbouring pixel tiles)
+    a.units = (cl == 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
     a.bx = p.bx;
     a.by = p.by;
     a.tiles_x = p.tiles_x;
@@ -556,7 +587,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
     a.ws = reinterpret_cast<float*>(wsb + p.part_off);
     a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
-    a.trace = g_trace_on & 15;
+    a.trace = g_trace_on & 15;  // bit0 trace, bit1 hi*hi only, bit2 no B split, bit3 no A->TMEM (experiments)
     a.relayout = (g_trace_on & 16) ? 0 : relayout;
     a.x = x;
     a.xh = reinterpret_cast<float*>(wsb + p.nhwc_off);
@@ -564,8 +595,9 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.wp = p.wp;
     a.pad = d->pad;
     a.gbar = reinterpret_cast<unsigned long long*>(wsb + p.gbar_off);
-    const int grid = std::min(a.units, occ * num_sms());
-    cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, tm_pix, tm_flt, a);
+    a.flt_early = t->prepared ? 1 : 0;  // b2c_conv_prepare synchronises, so a prepared pack is complete
+    const int grid = cl == 2 ? 2 * std::min(a.units, num_sms() / 2) : std::min(a.units, occ * num_sms());
+    cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, cl, tm_pix, tm_flt, a);
     if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
     return B2C_OK;
 }
@@ -697,6 +729,11 @@ int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, 
     if (rc) return rc;
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return cuda_fail(le, "pack launch");
+    // One-time setup call: complete the pack before returning, so that later
+    // launches with prepared != 0 may read it without ordering on the stream
+    // (the TMA kernel fetches filters ahead of griddepcontrol.wait).
+    le = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    if (le != cudaSuccess) return cuda_fail(le, "pack synchronize");
     return B2C_OK;
 }
 

@@ -72,8 +72,9 @@ constexpr int TM_HDR = 2048;           // barriers, TMEM slot, flags (< 1 KB); u
 constexpr int TM_MAX_SMEM = 232448;    // 227 KB opt-in per CTA
 constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 
-template <int BN, bool SWAP, int MODE, int OCC = 1>
+template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1>
 struct TmaCfg {
+    static_assert(CL == 1 || (CL == 2 && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
     // drain warp groups (column halves); two groups halve the exposed epilogue
@@ -121,6 +122,7 @@ struct TArgs {
     int* sems;          // split-K tickets [tile], zero at rest
     int split, kps, kblocks;
     int tiles_n;        // filter tiles
+    int tiles_m;        // pixel tiles
     int units;          // pixel tiles * filter tiles * split
     int bx, by;         // MODE 4: output-pixel block of a tile (bx * by <= 128 rows)
     int tiles_x, tiles_y;  // MODE 4: blocks per image row / column
@@ -135,19 +137,26 @@ struct TArgs {
     float* xh;
     int hp, wp, pad;
     unsigned long long* gbar;  // grid barrier counter (monotonic; zero at allocation)
+    int flt_early;      // packed filters are complete: the loader may fetch them before griddepcontrol.wait
 };
 
 struct Unit {
     int t, m0, n0, z, kb_begin, nkb;
     int b, oy0, ox0;  // MODE 4 tile origin
+    bool ghost;       // 2-CTA pair whose second pixel tile is past the end: runs the pipeline, stores nothing
 };
 
-template <int PIX_ROWS, int FLT_ROWS, int MODE>
-__device__ __forceinline__ Unit unit_of(const TArgs& a, int u) {
+// Unit u of a CTA (CL = 1), or pair-unit u of a 2-CTA cluster (CL = 2: the two
+// CTAs take pixel tiles 2p and 2p+1 with the same filter tile and K range).
+template <int PIX_ROWS, int FLT_ROWS, int MODE, int CL = 1>
+__device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     Unit w;
     w.z = u % a.split;
-    w.t = u / a.split;
-    const int nt = w.t % a.tiles_n, mt = w.t / a.tiles_n;
+    const int t2 = u / a.split;
+    const int nt = t2 % a.tiles_n;
+    const int mt = CL == 2 ? 2 * (t2 / a.tiles_n) + rank : t2 / a.tiles_n;
+    w.ghost = mt >= a.tiles_m;
+    w.t = mt * a.tiles_n + nt;
     w.m0 = mt * PIX_ROWS;
     w.n0 = nt * FLT_ROWS;
     w.kb_begin = w.z * a.kps;
@@ -285,6 +294,18 @@ __device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
+}
+
+// One K block of packed filters into a stage: one bulk copy, or, in a 2-CTA
+// pair, each CTA fetches half (raw | lo) and multicasts it to both.
+template <int BYTES, int CL>
+__device__ __forceinline__ void load_filters(uint32_t dst, const char* src, uint32_t bar, int rank) {
+    if (CL == 2) {
+        constexpr uint32_t H = BYTES / 2;
+        bulk_g2s_mc(dst + (uint32_t)rank * H, src + (size_t)rank * H, H, bar, (uint16_t)0x3);
+    } else {
+        bulk_g2s(dst, src, BYTES, bar);
+    }
 }
 
 // ----------------------------------------------------------------------------- split + epilogue helpers
@@ -445,10 +466,10 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
 
 // ----------------------------------------------------------------------------- main kernel
 
-template <int BN, bool SWAP, int MODE, int OCC>
-__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
+template <int BN, bool SWAP, int MODE, int OCC, int CL>
+__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
     k_tconv(const __grid_constant__ CUtensorMap tm_pix, const __grid_constant__ CUtensorMap tm_flt, TArgs a) {
-    using Cfg = TmaCfg<BN, SWAP, MODE, OCC>;
+    using Cfg = TmaCfg<BN, SWAP, MODE, OCC, CL>;
     constexpr int STAGES = Cfg::STAGES;
     constexpr int DC = Cfg::DRAIN_COLS;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -467,13 +488,15 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int G = a.drain;
+    const int rank = CL == 2 ? (int)cluster_ctarank() : 0;
+    const int ubase = (int)blockIdx.x / CL, ustride = (int)gridDim.x / CL;
     if (tid == 0) B2C_TRACE(a.trace, 0);
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&raw_full[s]), 1);
             mbar_init(smem_u32(&split_full[s]), TM_SPLIT_THREADS);
-            mbar_init(smem_u32(&empty_bar[s]), 1);
+            mbar_init(smem_u32(&empty_bar[s]), CL);  // one tcgen05.commit per CTA of the pair
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull_bar[s]), 1);
@@ -489,11 +512,16 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
     }
     tc_fence_before();
     __syncthreads();
+    if (CL == 2) cluster_sync_all();  // the peer's barriers exist before any multicast reaches them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (tid == 0) B2C_TRACE(a.trace, 1);
     pdl_launch_dependents();
-    pdl_wait();
+    // The loader may stream the first stages' packed filters (constant, written
+    // by an earlier synchronised b2c_conv_prepare) while the previous kernel
+    // (the x re-layout) is still running; everything else waits for it here.
+    const bool early = a.flt_early && MODE != 1 && !a.relayout && warp == Cfg::LOAD_WARP;
+    if (!early) pdl_wait();
     if (a.relayout) fused_relayout(a, smem + TM_HDR + 1024);
     if (tid == 0) B2C_TRACE(a.trace, 3);
 
@@ -502,8 +530,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
         int stage = 0, n = 0;
         uint32_t phase = 0;
         const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);  // this warp's 32 TMEM lanes
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+        for (int u = ubase; u < a.units; u += ustride) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
             for (int i = 0; i < w.nkb; ++i, ++n) {
                 const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
                 mbar_wait(smem_u32(&raw_full[stage]), phase);
@@ -513,7 +541,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
                     mbar_wait(smem_u32(&afree_bar[aslot]), (uint32_t)((n / Cfg::A_SLOTS) - 1) & 1u);
                 tc_fence_after();
                 const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + aslot * 64);
-                a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);
+                if (!(a.trace & 8)) a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);  // debug bit 3: skip
                 if (Cfg::B_SPLIT && !(a.trace & 4)) split_tile<BN>(sbase + Cfg::A_SMEM, tid);
                 fence_proxy_async_smem();
                 tmem_st_wait();
@@ -534,8 +562,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
         const int row = quarter * 32 + lane;  // TMEM lane = MMA M row
         const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c_begin;
         int cidx = 0;
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+        for (int u = ubase; u < a.units; u += ustride) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
             float acc[DC];
 #pragma unroll
             for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
@@ -550,10 +578,11 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&tempty_bar[slot]));
             }
-            if (dtid == 0 && u == (int)blockIdx.x) B2C_TRACE(a.trace, 4);
-            const int ui = (u - (int)blockIdx.x) / (int)gridDim.x;
+            if (dtid == 0 && u == ubase) B2C_TRACE(a.trace, 4);
+            const int ui = (u - ubase) / ustride;
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 208 + 2 * ui);
-            epilogue_unit<BN, SWAP, DC, Cfg::DRAIN_THREADS, MODE>(a, w, acc, c_begin, row, dtid, last_flag, bias_s, bpre);
+            if (!w.ghost)
+                epilogue_unit<BN, SWAP, DC, Cfg::DRAIN_THREADS, MODE>(a, w, acc, c_begin, row, dtid, last_flag, bias_s, bpre);
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 209 + 2 * ui);
         }
         if (dtid == 0) B2C_TRACE(a.trace, 6);
@@ -562,8 +591,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
         constexpr uint32_t idesc = umma_idesc(2, TM_M, BN);
         int stage = 0, cidx = 0, n = 0;
         uint32_t phase = 0;
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+        for (int u = ubase; u < a.units; u += ustride) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
             int kin = 0;
             for (int i = 0; i < w.nkb; ++i, ++n) {
                 const int slot = cidx & 1;
@@ -600,7 +629,10 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
                             mma_tf32_ts(d, a_lo + 8 * s, dbh, idesc, 1u);
                         }
                     }
-                    tc_commit(smem_u32(&empty_bar[stage]));
+                    if (CL == 2)  // the stage's filter half may be refilled by either CTA
+                        tc_commit_mc(smem_u32(&empty_bar[stage]), (uint16_t)0x3);
+                    else
+                        tc_commit(smem_u32(&empty_bar[stage]));
                     tc_commit(smem_u32(&afree_bar[n % Cfg::A_SLOTS]));
                     if (last) tc_commit(smem_u32(&tfull_bar[slot]));
                     if (n < 32) B2C_TRACE(a.trace, 144 + n);
@@ -623,8 +655,24 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
         // ------------------------------------------------------------ TMA / bulk loader
         int stage = 0, n = 0;
         uint32_t phase = 0;
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE>(a, u);
+        int npre = 0;  // stages whose filter bytes were issued before griddepcontrol.wait
+        if (early) {
+            if (ubase < a.units) {
+                const Unit w0 = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase, rank);
+                npre = min(STAGES, w0.nkb);
+                const char* wsrc0 = reinterpret_cast<const char*>(a.wpk) +
+                                    ((size_t)(w0.n0 / Cfg::FLT_ROWS) * a.kblocks + w0.kb_begin) * (size_t)Cfg::FLT_STAGE;
+                for (int i = 0; i < npre; ++i) {
+                    const uint32_t bar = smem_u32(&raw_full[i]);
+                    mbar_expect_tx(bar, Cfg::FLT_STAGE);
+                    load_filters<Cfg::FLT_STAGE, CL>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
+                                                    wsrc0 + (size_t)i * Cfg::FLT_STAGE, bar, rank);
+                }
+            }
+            pdl_wait();
+        }
+        for (int u = ubase; u < a.units; u += ustride) {
+            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
             int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
             if (MODE == 0 || MODE == 3) {
                 uint32_t b, p, oy, ox;
@@ -644,7 +692,10 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
                 const int kb = w.kb_begin + i;
                 // MODE 4 boxes are bx*by rows (<= 128): the rest of the tile keeps
                 // stale (finite) data whose output rows the epilogue discards.
-                mbar_arrive_expect_tx(bar, MODE == 4 ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u : Cfg::BYTES);
+                const bool pre = n < npre;  // filter bytes already issued (and counted) for this stage
+                const uint32_t bytes = (MODE == 4 ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u : Cfg::BYTES) -
+                                       (pre ? (uint32_t)Cfg::FLT_STAGE : 0u);
+                mbar_arrive_expect_tx(bar, bytes);
                 if (n < 32) B2C_TRACE(a.trace, 176 + n);
                 if (MODE == 1) {
                     tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
@@ -675,7 +726,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
                                                (uint16_t)kx, (uint16_t)ky);
                         }
                     }
-                    bulk_g2s(sbase + Cfg::FLT_OFF, wsrc + (size_t)i * Cfg::FLT_STAGE, Cfg::FLT_STAGE, bar);
+                    if (!pre) load_filters<Cfg::FLT_STAGE, CL>(sbase + Cfg::FLT_OFF, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
                 }
                 if (++stage == STAGES) {
                     stage = 0;
@@ -686,6 +737,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC>::THREADS, OCC)
     }
     if (tid == 0) B2C_TRACE(a.trace, 2);
     __syncthreads();
+    if (CL == 2) cluster_sync_all();  // no multicast or remote commit may still target this CTA
     if (warp == Cfg::MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);

@@ -55,6 +55,7 @@ class TuneParams:
     drain: int = 0  # K blocks per TMEM chunk before the fp32 register drain (0 = library default)
     tma: int = 0  # tcgen05: 1 = TMA-fed kernel (im2col on an NHWC copy / 2-D tiles), 2 = 2-D tiles for 1x1; 0 = warp gathers
     occ: int = 1  # TMA kernel: CTAs per SM (2 needs bn <= 64)
+    cl: int = 1  # TMA kernel: 2 = CTA pairs sharing (multicasting) the filter stages
 
     def __post_init__(self):
         if min(self.mnt) < 1 or min(self.mnb) < 1 or self.kb < 1:
@@ -76,7 +77,7 @@ class TuneParams:
         return (f"MNt={self.mnt[0]}:{self.mnt[1]},MNb={self.mnb[0]}:{self.mnb[1]},Kb={self.kb},vw={self.vw},"
                 f"lf={int(self.use_local_filts)},li={int(self.use_local_in)},"
                 f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)},dr={self.drain}"
-                + (f",tm={int(self.tma)}" if self.tma else "") + (f",oc={self.occ}" if self.occ != 1 else ""))
+                + (f",tm={int(self.tma)}" if self.tma else "") + (f",oc={self.occ}" if self.occ != 1 else "") + (f",cl={self.cl}" if self.cl != 1 else ""))
 
     @staticmethod
     def from_string(text: str) -> "TuneParams":
@@ -96,6 +97,7 @@ class TuneParams:
                 drain=int(kv.get("dr", "0")),
                 tma=int(kv.get("tm", "0")),
                 occ=int(kv.get("oc", "1")),
+                cl=int(kv.get("cl", "1")),
             )
         except (KeyError, ValueError) as e:
             raise CuclgenError(f"bad tune-params string {text!r}: {e}") from None
@@ -175,7 +177,7 @@ class Variant:
     def tune_struct(self, params: TuneParams) -> backend.Tune:
         return backend.Tune(self.vid, params.mnt[0], params.mnt[1], params.mnb[0], params.mnb[1], params.kb,
                             params.vw, params.bn, params.occ if params.tma else 0, params.split_k,
-                            int(params.swap_ab), params.drain, 0, int(params.tma))
+                            int(params.swap_ab), params.drain, 0, int(params.tma), params.cl)
 
     def applies(self, node: OpNode, edges, params: TuneParams) -> str | None:
         """None when applicable, else the reason (variants.py:206-210).  The C
@@ -271,6 +273,8 @@ class _UmmaFamily(Variant):
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
                         if tma and bn <= 64:
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))
+                        if tma and not swap and self.name != "conv_fc" and bn >= 64:
+                            out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

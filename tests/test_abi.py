@@ -50,7 +50,7 @@ def _desc(**kw):
 
 
 def _tune(variant, **kw):
-    t = dict(mnt0=4, mnt1=4, mnb0=16, mnb1=16, kb=4, vw=4, tile_n=128, stages=0, split_k=1, swap_ab=0, drain=0, prepared=0, tma=0)
+    t = dict(mnt0=4, mnt1=4, mnb0=16, mnb1=16, kb=4, vw=4, tile_n=128, stages=0, split_k=1, swap_ab=0, drain=0, prepared=0, tma=0, cluster=0)
     t.update(kw)
     return backend.Tune(variant, *t.values())
 

@@ -58,7 +58,8 @@ def _variant_params(g):
                     TuneParams(bn=96, swap_ab=True, split_k=3, tma=True), TuneParams(bn=64, tma=2),
                     TuneParams(bn=32, swap_ab=True, split_k=2, tma=2), TuneParams(bn=96, tma=2),
                     TuneParams(bn=32, split_k=2, tma=1), TuneParams(bn=64, tma=1, occ=2),
-                    TuneParams(bn=32, swap_ab=True, split_k=2, tma=1, occ=2)):
+                    TuneParams(bn=32, swap_ab=True, split_k=2, tma=1, occ=2), TuneParams(bn=64, tma=1, cl=2),
+                    TuneParams(bn=96, split_k=2, tma=2, cl=2)):
             out.append((v, prm))
     return [(n, p) for n, p in out if VARIANTS[n].applies(node, g.edges, p) is None]
 
@@ -203,7 +204,7 @@ def test_bad_args_raise(cuda):
     from paper_1611_06945_b200.errors import ShapeMismatch
 
     d = backend.make_desc(1, 3, 8, 8, 4, 3, 1, 1, 7, 8, False)  # wrong oh
-    t = backend.Tune(backend.VAR_SIMPLE, 1, 1, 1, 1, 1, 1, 32, 0, 1, 0, 0, 0, 0)
+    t = backend.Tune(backend.VAR_SIMPLE, 1, 1, 1, 1, 1, 1, 32, 0, 1, 0, 0, 0, 0, 0)
     z = torch.zeros(1024, device="cuda")
     with pytest.raises(ShapeMismatch):
         backend.fwd(d, t, z, z, z, z)
