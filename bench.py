@@ -58,6 +58,10 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="multi-GPU: split each op's batch across ranks (strong scaling) instead of N images per rank")
+    ap.add_argument("--gather", action="store_true",
+                    help="multi-GPU: all-gather every op's output slabs over NCCL inside the timed step")
     ap.add_argument("--debug-flags", type=int, default=0,
                     help="library debug flags (measurement experiments only; results are then not valid bench lines)")
     return ap.parse_args()
@@ -119,14 +123,23 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_sweep(batches, db, heuristic, rank):
-    """(row, BenchOp, node, edges, variant, params) for every op of the sweep."""
+def build_sweep(batches, db, heuristic, rank, world=1, strong=False):
+    """(row, BenchOp, node, edges, variant, params) for every op of the sweep.
+    Weak scaling: every rank runs every op on its own N images.  Strong
+    scaling: rank r takes its contiguous slab of each op's N images
+    (shard.batch_slab); ops whose slab is empty on this rank are skipped."""
     from paper_1611_06945_b200 import corpus
     from paper_1611_06945_b200.frontend import with_fused
+    from paper_1611_06945_b200.shard import batch_slab
     from paper_1611_06945_b200.variants import select_variant
 
     out = []
     for row, op in corpus.sweep_ops(batches):
+        if strong and world > 1:
+            n_local = batch_slab(op.batch, world, rank)[1]
+            if n_local == 0:
+                continue
+            op = op.with_batch(n_local)
         g = with_fused(op.graph(), "conv", "relu")
         node = g.node("conv")
         v, params = select_variant(node, g.edges, None if heuristic else db)
@@ -217,7 +230,7 @@ def run_ours(args, rank, world, local_rank):
     batches = [int(b) for b in args.batches.split(",")]
     db_path = args.db or tuner.shipped_db_path()
     db = tuner.load_db(db_path) if (os.path.exists(db_path) and not args.heuristic) else None
-    sweep = build_sweep(batches, db, args.heuristic, rank)
+    sweep = build_sweep(batches, db, args.heuristic, rank, world, args.strong)
 
     ops, hosts, rows = [], [], []
     for row, op, node, edges, v, params in sweep:
@@ -257,8 +270,18 @@ def run_ours(args, rank, world, local_rank):
                 evs[i + 1].record(stream)
     torch.cuda.synchronize()
 
+    gather = args.gather and world > 1
+    if gather:
+        from paper_1611_06945_b200.shard import gather_batch
+        if args.strong:
+            raise SystemExit("--gather is implemented for weak scaling (every rank holds every op)")
+        n_fulls = [world * op.batch for (_, op, _, _, _) in rows]  # all ranks' images of each op
     for _ in range(args.warmup):
         graph.replay()
+        if gather:
+            with torch.cuda.stream(stream):
+                for o, n_full in zip(ops, n_fulls):
+                    gather_batch(o.y, n_full)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -272,7 +295,9 @@ def run_ours(args, rank, world, local_rank):
             t0.record(stream)
             for _ in range(args.steps):
                 graph.replay()
-                # per-op durations of this replay, read after the region (events are in the graph)
+                if gather:
+                    for o, n_full in zip(ops, n_fulls):
+                        gather_batch(o.y, n_full)
             t1.record(stream)
         torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
@@ -287,7 +312,12 @@ def run_ours(args, rank, world, local_rank):
         tt = torch.tensor([ms_step], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_step = float(tt.item())
-    value = world * flops_step / (ms_step * 1e-3) / 1e12
+    flops_all = world * flops_step
+    if world > 1 and args.strong:  # ranks hold different slabs: sum the work actually done
+        ft = torch.tensor([float(flops_step)], device=dev, dtype=torch.float64)
+        dist.all_reduce(ft, op=dist.ReduceOp.SUM)
+        flops_all = float(ft.item())
+    value = flops_all / (ms_step * 1e-3) / 1e12
 
     # ---- e2e through the host-buffer C call
     e2e = None
@@ -366,9 +396,12 @@ def run_ours(args, rank, world, local_rank):
         e[1] += conv_flops(ops[i].plan.desc)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong" if (args.strong and world > 1) else "weak",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": ",".join(str(b * world) for b in batches),
+        "config": {"workload": WORKLOAD,
+                   "global_batch": ",".join(str(b if args.strong else b * world) for b in batches),
+                   "sharding": "batch slabs per op (strong)" if args.strong else "N images per rank (weak)",
+                   "output_gather": "NCCL all_gather of every op's slabs, inside the timed step" if gather else "none",
                    "ops_per_step": n, "flops_per_step_per_gpu": flops_step, "parallelism": f"batch-shard x{world}",
                    "variant_source": "heuristic" if db is None else os.path.relpath(db_path, ROOT),
                    "l2": "working set ~0.6 GB > 126 MB L2 (no explicit flush)",
