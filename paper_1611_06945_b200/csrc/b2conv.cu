@@ -150,7 +150,8 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     }
     // tcgen05 family
     if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192"; return B2C_INAPPLICABLE; }
-    if (t->split_k < 1) { why = "split_k must be >= 1"; return B2C_BAD_ARGS; }
+    if (t->split_k < 0 || (t->split_k == 0 && !t->tma)) { why = "split_k must be >= 1 (0 = stream-K, TMA kernel only)"; return B2C_BAD_ARGS; }
+    if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K is single-CTA"; return B2C_INAPPLICABLE; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
     if (t->tma < 0 || t->tma > 2) { why = "tma must be 0, 1 or 2"; return B2C_BAD_ARGS; }
@@ -183,6 +184,7 @@ struct UmmaPlan {
     int grid_x, grid_y, split, kps, kblocks, cblocks, tiles, kmode, flt_rows, tma;
     int bx, by, tiles_x, tiles_y, hp, wp;  // kmode 5: pixel blocks and the padded NHWC extent
     int parts;                             // packed filter halves per K block (2: raw | lo, 1: raw)
+    int streamk, sk_grid, sk_maxc;         // split_k == 0: stream-K over the units' K blocks
     size_t wpk_bytes;   // packed filters (offset 0 of the workspace; 0 for the TMA fc path)
     size_t part_off;    // split-K partials
     size_t sems_off;    // split-K tickets
@@ -192,6 +194,8 @@ struct UmmaPlan {
 };
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+int num_sms();
 
 UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     UmmaPlan p;
@@ -223,10 +227,19 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     // packed filters: raw | lo per K block; raw only when the TMA kernel takes them as its TMEM A operand
     p.parts = (p.tma && t->swap_ab) ? 1 : 2;
     p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * p.parts * p.flt_rows * UMMA_BK * sizeof(float);
+    p.streamk = (t->tma && t->split_k == 0) ? 1 : 0;
+    p.sk_grid = p.sk_maxc = 0;
+    size_t nslots = p.split > 1 ? (size_t)p.tiles * p.split : 0;
+    if (p.streamk) {
+        const long long W = (long long)p.tiles * p.kblocks;
+        p.sk_grid = (int)std::min<long long>(W, num_sms());
+        const long long L = std::max<long long>(1, W / p.sk_grid);  // K blocks per CTA (floor)
+        p.sk_maxc = (int)((p.kblocks + L - 1) / L + 1);
+        nslots = (size_t)p.tiles * p.sk_maxc;
+    }
     p.part_off = align256(p.wpk_bytes);
-    p.sems_off = p.part_off;
-    if (p.split > 1) p.sems_off += align256((size_t)p.tiles * p.split * BN * UMMA_M * sizeof(float));
-    p.nhwc_off = p.sems_off + (p.split > 1 ? align256((size_t)p.tiles * sizeof(int)) : 0);
+    p.sems_off = p.part_off + (nslots ? align256(nslots * BN * UMMA_M * sizeof(float)) : 0);
+    p.nhwc_off = p.sems_off + (nslots ? align256((size_t)p.tiles * sizeof(int)) : 0);
     const bool nhwc = p.tma && (p.kmode == 3 || p.kmode == 4 || p.kmode == 5);
     const int cp = p.kmode >= 4 ? 4 : d->c;  // first layers: channels padded to 4 (16-byte pixels)
     const size_t pix = p.kmode == 5 ? (size_t)p.hp * p.wp : (size_t)d->h * d->w;
@@ -567,7 +580,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         rc = encode_rows(&tm_flt, w, d->k, (long long)g.K, t->swap_ab ? TM_M : t->tile_n);
         if (rc) return rc;
     }
-    TArgs a;
+    TArgs a = {};  // every field set below; zero-init guards new ones
     a.g = g;
     a.wpk = reinterpret_cast<const float*>(ws);
     a.bias = bias;
@@ -575,6 +588,8 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.split = p.split;
     a.kps = p.kps;
     a.kblocks = p.kblocks;
+    a.streamk = p.streamk;
+    a.sk_maxc = p.sk_maxc;
     a.tiles_n = p.grid_y;
     a.tiles_m = p.grid_x;
     // CL = 2: units are pair-units (two neighbouring pixel tiles)
@@ -596,7 +611,9 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.pad = d->pad;
     a.gbar = reinterpret_cast<unsigned long long*>(wsb + p.gbar_off);
     a.flt_early = t->prepared ? 1 : 0;  // b2c_conv_prepare synchronises, so a prepared pack is complete
-    const int grid = cl == 2 ? 2 * std::min(a.units, num_sms() / 2) : std::min(a.units, occ * num_sms());
+    const int grid = p.streamk ? p.sk_grid
+                     : cl == 2  ? 2 * std::min(a.units, num_sms() / 2)
+                                : std::min(a.units, occ * num_sms());
     cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, cl, tm_pix, tm_flt, a);
     if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
     return B2C_OK;

@@ -121,6 +121,8 @@ struct TArgs {
     float* ws;          // split-K partials [tile][split][BN][128]
     int* sems;          // split-K tickets [tile], zero at rest
     int split, kps, kblocks;
+    int streamk;        // 1: every CTA takes an equal contiguous range of the units' K blocks (split == 1)
+    int sk_maxc;        // stream-K: partial slots per unit (max CTAs sharing one unit)
     int tiles_n;        // filter tiles
     int tiles_m;        // pixel tiles
     int units;          // pixel tiles * filter tiles * split
@@ -140,8 +142,30 @@ struct TArgs {
     int flt_early;      // packed filters are complete: the loader may fetch them before griddepcontrol.wait
 };
 
+// Walks a CTA's work: units blockIdx, +stride, ... ; or, in stream-K mode, the
+// contiguous K-block range [c*W/G, (c+1)*W/G) of the W = units*kblocks K
+// blocks, cut into per-unit segments.  A unit whose K blocks span several CTAs
+// is finished through the split-K partials (contributors in CTA order).
+struct UnitCursor {
+    long long k, end;
+    int u;
+};
+
+__device__ __forceinline__ long long sk_start(long long W, int G, int c) { return (long long)c * W / G; }
+
+template <int PIX_ROWS, int FLT_ROWS, int MODE, int CL>
+__device__ __forceinline__ UnitCursor cursor_begin(const TArgs& a, int ubase) {
+    UnitCursor c;
+    c.u = ubase;
+    const long long W = (long long)a.units * a.kblocks;
+    c.k = sk_start(W, gridDim.x, blockIdx.x);
+    c.end = sk_start(W, gridDim.x, blockIdx.x + 1);
+    return c;
+}
+
 struct Unit {
     int t, m0, n0, z, kb_begin, nkb;
+    int nsplit, pslot0;  // contributors to this tile's output (1 = direct store); first partial slot
     int b, oy0, ox0;  // MODE 4 tile origin
     bool ghost;       // 2-CTA pair whose second pixel tile is past the end: runs the pipeline, stores nothing
 };
@@ -170,7 +194,41 @@ __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     } else {
         w.b = w.oy0 = w.ox0 = 0;
     }
+    w.nsplit = a.split;
+    w.pslot0 = w.t * a.split;
     return w;
+}
+
+template <int PIX_ROWS, int FLT_ROWS, int MODE, int CL>
+__device__ __forceinline__ bool next_unit(const TArgs& a, UnitCursor& cur, int ustride, int rank, Unit& w) {
+    if (a.streamk) {
+        if (cur.k >= cur.end) return false;
+        const int u = (int)(cur.k / a.kblocks);
+        const int kb0 = (int)(cur.k - (long long)u * a.kblocks);
+        const long long left = cur.end - cur.k;
+        const int n = (int)(left < (long long)(a.kblocks - kb0) ? left : (long long)(a.kblocks - kb0));
+        w = unit_of<PIX_ROWS, FLT_ROWS, MODE, CL>(a, u, rank);
+        w.kb_begin = kb0;
+        w.nkb = n;
+        // CTAs owning this unit's first and last K block
+        const long long W = (long long)a.units * a.kblocks;
+        const int G = gridDim.x;
+        const long long x0 = (long long)u * a.kblocks, x1 = x0 + a.kblocks - 1;
+        int c0 = (int)(x0 * G / W), c1 = (int)(x1 * G / W);
+        while (c0 + 1 < G && sk_start(W, G, c0 + 1) <= x0) ++c0;
+        while (c0 > 0 && sk_start(W, G, c0) > x0) --c0;
+        while (c1 + 1 < G && sk_start(W, G, c1 + 1) <= x1) ++c1;
+        while (c1 > 0 && sk_start(W, G, c1) > x1) --c1;
+        w.nsplit = c1 - c0 + 1;
+        w.z = (int)blockIdx.x - c0;
+        w.pslot0 = w.t * a.sk_maxc;
+        cur.k += n;
+        return true;
+    }
+    if (cur.u >= a.units) return false;
+    w = unit_of<PIX_ROWS, FLT_ROWS, MODE, CL>(a, cur.u, rank);
+    cur.u += ustride;
+    return true;
 }
 
 // ----------------------------------------------------------------------------- NCHW -> NHWC
@@ -378,15 +436,15 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
         if (dtid < BN) bias_s[dtid] = bpre;
         named_bar_sync(1, NT);
     }
-    if (a.split > 1) {
-        float* part = a.ws + ((size_t)w.t * a.split + w.z) * BN * TM_M;
+    if (w.nsplit > 1) {
+        float* part = a.ws + ((size_t)w.pslot0 + w.z) * BN * TM_M;
 #pragma unroll
         for (int j = 0; j < DC; ++j) __stcg(part + (size_t)(c_begin + j) * TM_M + row, acc[j]);
         __threadfence();
         named_bar_sync(1, NT);
         if (dtid == 0) {
             const int ticket = atomicAdd(a.sems + w.t, 1);
-            *last_flag = (ticket == a.split - 1);
+            *last_flag = (ticket == w.nsplit - 1);
         }
         named_bar_sync(1, NT);
         const bool last = *last_flag != 0;
@@ -394,10 +452,10 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
         if (!last) return;
         __threadfence();
         if (dtid == 0) a.sems[w.t] = 0;
-        const float* base = a.ws + (size_t)w.t * a.split * BN * TM_M;
+        const float* base = a.ws + (size_t)w.pslot0 * BN * TM_M;
 #pragma unroll
         for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
-        for (int zz = 0; zz < a.split; ++zz) {
+        for (int zz = 0; zz < w.nsplit; ++zz) {
 #pragma unroll
             for (int j = 0; j < DC; ++j) acc[j] += __ldcg(base + ((size_t)zz * BN + c_begin + j) * TM_M + row);
         }
@@ -530,8 +588,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
         int stage = 0, n = 0;
         uint32_t phase = 0;
         const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);  // this warp's 32 TMEM lanes
-        for (int u = ubase; u < a.units; u += ustride) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
+        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
             for (int i = 0; i < w.nkb; ++i, ++n) {
                 const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
                 mbar_wait(smem_u32(&raw_full[stage]), phase);
@@ -561,9 +619,10 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
         const int dtid = tid - 128;
         const int row = quarter * 32 + lane;  // TMEM lane = MMA M row
         const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c_begin;
+        int ui = 0;  // unit ordinal (trace slots)
         int cidx = 0;
-        for (int u = ubase; u < a.units; u += ustride) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
+        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
             float acc[DC];
 #pragma unroll
             for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
@@ -578,12 +637,12 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&tempty_bar[slot]));
             }
-            if (dtid == 0 && u == ubase) B2C_TRACE(a.trace, 4);
-            const int ui = (u - ubase) / ustride;
+            if (dtid == 0 && ui == 0) B2C_TRACE(a.trace, 4);
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 208 + 2 * ui);
             if (!w.ghost)
                 epilogue_unit<BN, SWAP, DC, Cfg::DRAIN_THREADS, MODE>(a, w, acc, c_begin, row, dtid, last_flag, bias_s, bpre);
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 209 + 2 * ui);
+            ++ui;
         }
         if (dtid == 0) B2C_TRACE(a.trace, 6);
     } else if (warp == Cfg::MMA_WARP) {
@@ -591,8 +650,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
         constexpr uint32_t idesc = umma_idesc(2, TM_M, BN);
         int stage = 0, cidx = 0, n = 0;
         uint32_t phase = 0;
-        for (int u = ubase; u < a.units; u += ustride) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
+        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
             int kin = 0;
             for (int i = 0; i < w.nkb; ++i, ++n) {
                 const int slot = cidx & 1;
@@ -657,8 +716,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
         uint32_t phase = 0;
         int npre = 0;  // stages whose filter bytes were issued before griddepcontrol.wait
         if (early) {
-            if (ubase < a.units) {
-                const Unit w0 = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase, rank);
+            UnitCursor c0 = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+            Unit w0;
+            if (next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, c0, ustride, rank, w0)) {
                 npre = min(STAGES, w0.nkb);
                 const char* wsrc0 = reinterpret_cast<const char*>(a.wpk) +
                                     ((size_t)(w0.n0 / Cfg::FLT_ROWS) * a.kblocks + w0.kb_begin) * (size_t)Cfg::FLT_STAGE;
@@ -671,8 +731,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
             }
             pdl_wait();
         }
-        for (int u = ubase; u < a.units; u += ustride) {
-            const Unit w = unit_of<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, u, rank);
+        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
             int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
             if (MODE == 0 || MODE == 3) {
                 uint32_t b, p, oy, ox;

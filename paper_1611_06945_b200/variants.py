@@ -66,7 +66,7 @@ class TuneParams:
             raise CuclgenError(f"vector width must be one of 1,2,4,8, got {self.vw}")
         if self.mnt[1] % self.vw:
             raise CuclgenError(f"vector width {self.vw} must divide register block {self.mnt[1]}")
-        if self.bn < 1 or self.split_k < 1 or self.drain < 0:
+        if self.bn < 1 or self.split_k < 0 or self.drain < 0:  # split_k 0 = stream-K (TMA kernel)
             raise CuclgenError(f"bad tcgen05 tile params {self}")
 
     @property
@@ -266,15 +266,11 @@ class _UmmaFamily(Variant):
             for bn in UMMA_BN:
                 if bn > 2 * max(32, n_rows):
                     continue
-                for split in (1, 2, 4, 8, 16, 32):
+                for split in (1, 2, 4, 8, 16, 32, 0):  # 0 = stream-K (TMA kernel)
                     if split > 1 and kblocks // split < 2:
                         continue
-                    for tma in (1, 2, 0):
+                    for tma in ((1, 2) if split == 0 else (1, 2, 0)):
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
-                        if tma and bn <= 64:
-                            out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))
-                        if tma and not swap and self.name != "conv_fc" and bn >= 64:
-                            out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

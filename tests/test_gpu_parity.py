@@ -57,7 +57,8 @@ def _variant_params(g):
                     TuneParams(bn=64, split_k=2, tma=True), TuneParams(bn=192, tma=True),
                     TuneParams(bn=96, swap_ab=True, split_k=3, tma=True), TuneParams(bn=64, tma=2),
                     TuneParams(bn=32, swap_ab=True, split_k=2, tma=2), TuneParams(bn=96, tma=2),
-                    TuneParams(bn=32, split_k=2, tma=1), TuneParams(bn=64, tma=1, occ=2),
+                    TuneParams(bn=32, split_k=2, tma=1), TuneParams(bn=64, split_k=0, tma=1),
+                    TuneParams(bn=32, swap_ab=True, split_k=0, tma=1), TuneParams(bn=64, tma=1, occ=2),
                     TuneParams(bn=32, swap_ab=True, split_k=2, tma=1, occ=2), TuneParams(bn=64, tma=1, cl=2),
                     TuneParams(bn=96, split_k=2, tma=2, cl=2)):
             out.append((v, prm))
