@@ -166,6 +166,45 @@ const char* b2c_last_error(void);
 /* Library version string ("b2conv <semver> sm_100a"). */
 const char* b2c_version(void);
 
+/* ============================================================================
+ * Whole-network forward: the non-conv node kinds.
+ * In the reference these are further Variant generators whose kernels
+ * runner.run_graph hands to run_kernel (runner.py:200-249): pool_max
+ * (variants.py:688-741), activation (variants.py:744-775) and xpose
+ * (variants.py:778-827).  Same conventions as the conv entry points: fp32,
+ * caller-owned device buffers, asynchronous on `stream`, status codes above.
+ * ========================================================================== */
+
+/* Max pooling over img:chan:y:x (PoolParams, frontend.py:68-80): square window r,
+ * stride, pad < r; out-of-range taps never win (ref_pool_max pads with -inf,
+ * oracle.py:100-116).  oh/ow must equal window_out (frontend.py:441-442). */
+typedef struct b2c_pool_desc {
+    int32_t n, c, h, w;
+    int32_t r, stride, pad;
+    int32_t oh, ow;
+} b2c_pool_desc;
+int b2c_pool_max_fwd(const b2c_pool_desc* d, const float* x, float* y, void* stream);
+
+/* y[i] = (x[i] > 0) ? x[i] : 0 for i < n (Activation "relu", variants.py:744-775;
+ * ref_relu, oracle.py:119-121).  x == y (in place) is allowed. */
+int b2c_relu_fwd(const float* x, float* y, int64_t n, void* stream);
+
+/* Layout conversion (Xpose, variants.py:778-827 = ndarray.convert_format,
+ * ndarray.py:232-253): output dims in output order; for output dim i the
+ * same-named source dim has extent src_sizes[i] and element stride
+ * src_strides[i].  Output is dense row-major over out_sizes; an index past the
+ * source extent reads 0 (growth zero-pads), out_sizes smaller than src_sizes
+ * crop. */
+#define B2C_XPOSE_MAX_DIMS 8
+typedef struct b2c_xpose_desc {
+    int32_t ndim;
+    int32_t reserved;
+    int64_t out_sizes[B2C_XPOSE_MAX_DIMS];
+    int64_t src_sizes[B2C_XPOSE_MAX_DIMS];
+    int64_t src_strides[B2C_XPOSE_MAX_DIMS];
+} b2c_xpose_desc;
+int b2c_xpose(const b2c_xpose_desc* d, const float* x, float* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

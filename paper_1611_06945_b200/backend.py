@@ -41,7 +41,12 @@ EXPORTS = (
     "b2c_conv_launches",
     "b2c_last_error",
     "b2c_version",
+    "b2c_pool_max_fwd",
+    "b2c_relu_fwd",
+    "b2c_xpose",
 )
+
+XPOSE_MAX_DIMS = 8
 
 
 class ConvDesc(ctypes.Structure):
@@ -51,6 +56,17 @@ class ConvDesc(ctypes.Structure):
 class Tune(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "variant", "mnt0", "mnt1", "mnb0", "mnb1", "kb", "vw", "tile_n", "stages", "split_k", "swap_ab", "drain", "prepared", "tma", "cluster")]
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("n", "c", "h", "w", "r", "stride", "pad", "oh", "ow")]
+
+
+class XposeDesc(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("out_sizes", ctypes.c_int64 * XPOSE_MAX_DIMS),
+                ("src_sizes", ctypes.c_int64 * XPOSE_MAX_DIMS),
+                ("src_strides", ctypes.c_int64 * XPOSE_MAX_DIMS)]
 
 
 _lib = None
@@ -83,6 +99,9 @@ def lib():
         L.b2c_conv_bytes.argtypes = [P(ConvDesc)]
         L.b2c_conv_bytes.restype = ctypes.c_int64
         L.b2c_conv_launches.argtypes = [P(ConvDesc), P(Tune)]
+        L.b2c_pool_max_fwd.argtypes = [P(PoolDesc), vp, vp, vp]
+        L.b2c_relu_fwd.argtypes = [vp, vp, ctypes.c_int64, vp]
+        L.b2c_xpose.argtypes = [P(XposeDesc), vp, vp, vp]
         L.b2c_last_error.restype = ctypes.c_char_p
         L.b2c_version.restype = ctypes.c_char_p
         _lib = L
@@ -168,6 +187,46 @@ def time_ms(desc: ConvDesc, tune: Tune, x, w, bias, y, ws=None, warmup=3, reps=1
                              ctypes.byref(out))
     check(rc, "b2c_conv_time")
     return float(out.value)
+
+
+def _stream(stream):
+    torch = _require_cuda()
+    return stream if stream is not None else torch.cuda.current_stream().cuda_stream
+
+
+def pool_max_fwd(desc: PoolDesc, x, y, stream=None):
+    """Max pooling on device tensors (b2c_pool_max_fwd). Async."""
+    st = _stream(stream)
+    check(lib().b2c_pool_max_fwd(ctypes.byref(desc), x.data_ptr(), y.data_ptr(), st), "b2c_pool_max_fwd")
+
+
+def relu_fwd(x, y, stream=None):
+    """y = relu(x) over x.numel() fp32 elements (b2c_relu_fwd). Async."""
+    st = _stream(stream)
+    check(lib().b2c_relu_fwd(x.data_ptr(), y.data_ptr(), int(x.numel()), st), "b2c_relu_fwd")
+
+
+def xpose_desc(src_names, src_sizes, src_strides, dst_names, dst_sizes) -> XposeDesc:
+    """Descriptor of convert_format(src -> dst) for b2c_xpose: per output dim, the
+    extent and element stride of the same-named source dim."""
+    if set(src_names) != set(dst_names) or len(src_names) != len(dst_names):
+        raise ShapeMismatch(f"cannot convert {tuple(src_names)} to {tuple(dst_names)}")
+    if len(dst_names) > XPOSE_MAX_DIMS:
+        raise Unsupported(f"{len(dst_names)} dims > {XPOSE_MAX_DIMS}")
+    d = XposeDesc()
+    d.ndim = len(dst_names)
+    for i, name in enumerate(dst_names):
+        j = list(src_names).index(name)
+        d.out_sizes[i] = int(dst_sizes[i])
+        d.src_sizes[i] = int(src_sizes[j])
+        d.src_strides[i] = int(src_strides[j])
+    return d
+
+
+def xpose(desc: XposeDesc, x, y, stream=None):
+    """Layout conversion on device tensors (b2c_xpose). Async."""
+    st = _stream(stream)
+    check(lib().b2c_xpose(ctypes.byref(desc), x.data_ptr(), y.data_ptr(), st), "b2c_xpose")
 
 
 def alloc_workspace(desc: ConvDesc, tune: Tune, device=None):

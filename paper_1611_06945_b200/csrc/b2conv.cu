@@ -714,6 +714,11 @@ int flush_l2(cudaStream_t st) {
 
 }  // namespace
 
+namespace b2c {
+// shared with b2net.cu: one thread-local last-error slot for the whole library
+int set_last_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace b2c
+
 // ============================================================================ C ABI
 
 extern "C" {

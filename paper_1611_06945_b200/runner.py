@@ -187,3 +187,178 @@ class HostRun:
 
 def shape_of(node: OpNode, edges):
     return conv_shape(node, edges)
+
+
+# ============================================================================ whole-network forward
+# plan_graph / run_graph (cuclgen/runner.py:118-249) on
+# the B200.  Every node is one launch of a libb2conv kernel on one stream, so a
+# whole forward pass can be captured in a CUDA graph (GraphExec.launch).
+
+
+@dataclass
+class ExecPlan:
+    """Variant choices, kernel plans and the conversion-spliced graph
+    (runner.py:118-152)."""
+
+    graph: object
+    pre_graph: object
+    order: list
+    alloc: object
+    insts: dict
+    choices: dict
+    canonical_inputs: dict
+    canonical_output: dict
+
+
+@dataclass
+class NodeRun:
+    name: str
+    variant: str
+    params: object
+    report: CostReport
+    cost: float
+
+
+@dataclass
+class RunResult:
+    checksums: dict
+    node_runs: list = None
+    oracle_checks: dict = None
+    sink_buffers: dict = None
+
+    def __post_init__(self):
+        self.node_runs = [] if self.node_runs is None else self.node_runs
+        self.oracle_checks = {} if self.oracle_checks is None else self.oracle_checks
+        self.sink_buffers = {} if self.sink_buffers is None else self.sink_buffers
+
+
+def plan_graph(g, db=None, fuse: bool = True) -> ExecPlan:
+    """fuse_activations, per-node select_variant + generate, insert_conversions
+    for the variants' required formats (Xpose nodes for the conversions), then
+    schedule and allocate (runner.py:155-193)."""
+    from . import graphopt
+    from .frontend import KIND_CONVERT, KIND_INPUT
+    from .variants import DEFAULT_TUNE, VARIANTS, select_variant
+
+    if fuse:
+        g = graphopt.fuse_activations(g)
+    choices, fmts, insts, cin, cout = {}, {}, {}, {}, {}
+    for n in g.nodes:
+        if n.kind == KIND_INPUT:
+            continue
+        v, p = select_variant(n, g.edges, db)
+        choices[n.name] = (v, p)
+        fmts[n.name] = v.required_formats(n, g.edges, p)
+        insts[n.name] = v.generate(n, g.edges, p, STATIC)
+        cin[n.name], cout[n.name] = n.inputs, n.outputs[0]
+    g2 = graphopt.insert_conversions(g, fmts)
+    for n in g2.nodes:
+        if n.kind == KIND_CONVERT and n.name not in insts:
+            xp = VARIANTS["xpose"]
+            choices[n.name] = (xp, DEFAULT_TUNE)
+            insts[n.name] = xp.generate(n, g2.edges, DEFAULT_TUNE, STATIC)
+    order = [name for name in graphopt.schedule(g2) if g2.node(name).kind != KIND_INPUT]
+    return ExecPlan(g2, g, order, graphopt.alloc_plan(g2), insts, {k: (v.name, p) for k, (v, p) in choices.items()},
+                    cin, cout)
+
+
+def checksum_bytes(buf: bytes) -> str:
+    """First 16 hex digits of sha256 over the fp32 buffer (runner.py:196-197)."""
+    return hashlib.sha256(buf).hexdigest()[:16]
+
+
+class GraphExec:
+    """A planned graph bound to device memory: one dense fp32 buffer per edge
+    (alloc_plan), sources filled with the seeded reference noise
+    (runner.py:213-216), conv filters packed once.  ``launch()`` issues every
+    node in schedule order on one stream — capturable in a CUDA graph."""
+
+    def __init__(self, plan: ExecPlan, seed=0, device="cuda", low: float = 0.1, high: float = 1.0):
+        torch = _torch()
+        from .frontend import KIND_CONV
+
+        self.plan, g = plan, plan.graph
+        self.buffers = {}
+        for e, spec in g.edges.items():
+            self.buffers[e] = torch.empty(spec.sizes, dtype=torch.float32, device=device)
+        for e in g.sources:
+            spec = g.edges[e]
+            self.buffers[e].copy_(torch.from_numpy(noise(spec.names, spec.sizes, seed_for(f"{seed}:{e}"), low, high).to_np()))
+        self.ops = {}
+        for name in plan.order:
+            node = g.node(name)
+            if node.kind == KIND_CONV:
+                x, w, b = (self.buffers[e] for e in node.inputs)
+                self.ops[name] = ConvOp(plan.insts[name], x, w, b, y=self.buffers[node.outputs[0]])
+        torch.cuda.synchronize()
+
+    def launch_node(self, name: str, stream=None):
+        node = self.plan.graph.node(name)
+        if name in self.ops:
+            self.ops[name].launch(stream)
+            return
+        inst = self.plan.insts[name]
+        x, y = self.buffers[node.inputs[0]], self.buffers[node.outputs[0]]
+        if inst.variant == "pool_max":
+            backend.pool_max_fwd(inst.desc, x, y, stream)
+        elif inst.variant == "activation":
+            backend.relu_fwd(x, y, stream)
+        elif inst.variant == "xpose":
+            backend.xpose(inst.desc, x, y, stream)
+        else:
+            raise CuclgenError(f"node '{name}': no launcher for variant {inst.variant}")
+
+    def launch(self, stream=None):
+        for name in self.plan.order:
+            self.launch_node(name, stream)
+
+    def nda(self, edge: str) -> NdArray:
+        spec = self.plan.graph.edges[edge]
+        return nda_from_np(spec.names, self.buffers[edge].cpu().numpy())
+
+    @property
+    def flops(self) -> int:
+        return sum(op.flops for op in self.ops.values())
+
+
+def run_graph(g, seed=0, db=None, check=None, fuse: bool = True, engine=None, keep_sinks: bool = False) -> RunResult:
+    """Execute a whole graph on the B200 (runner.py:200-249): plan, allocate,
+    fill sources with seeded noise, launch every node in schedule order (each
+    timed with CUDA events into its CostReport), then checksum the sinks.
+
+    ``check``: the reference compares each node with its CPU oracle; the product
+    ships no CPU path, so the caller supplies the checker —
+    ``check(node, edges, inputs: dict[edge, NdArray], got: NdArray) -> result``
+    — and its results land in ``RunResult.oracle_checks``.  Each node is
+    checked against its canonical (pre-conversion) operand edges.  ``engine``
+    belongs to the reference's simulator and is accepted for signature
+    compatibility only."""
+    torch = _torch()
+    from dataclasses import replace as dc_replace
+
+    plan = plan_graph(g, db=db, fuse=fuse)
+    ex = GraphExec(plan, seed)
+    res = RunResult(checksums={})
+    for name in plan.order:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ex.launch_node(name)
+        e1.record()
+        e1.synchronize()
+        ns = int(e0.elapsed_time(e1) * 1e6)
+        vname, params = plan.choices[name]
+        res.node_runs.append(NodeRun(name, vname, params, CostReport(wall_ns=ns), float(ns)))
+    if check is not None:
+        g2 = plan.graph
+        for name in plan.order:
+            node = g2.node(name)
+            if name in plan.canonical_inputs:
+                node = dc_replace(node, inputs=plan.canonical_inputs[name], outputs=(plan.canonical_output[name],))
+            inputs = {e: ex.nda(e) for e in node.inputs}
+            res.oracle_checks[name] = check(node, g2.edges, inputs, ex.nda(node.outputs[0]))
+    for e in plan.graph.sinks:
+        arr = ex.buffers[e].cpu().numpy()
+        res.checksums[e] = checksum_bytes(arr.tobytes())
+        if keep_sinks:
+            res.sink_buffers[e] = nda_from_np(plan.graph.edges[e].names, arr)
+    return res

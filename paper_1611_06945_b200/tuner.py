@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 from .backend import CostReport
 from .errors import CuclgenError, Inapplicable
-from .frontend import KIND_CONV, ConvParams, OpNode, window_out
+from .frontend import KIND_ACT, KIND_CONV, KIND_CONVERT, KIND_POOL, ConvParams, OpNode, window_out
 from .variants import VARIANTS, TuneParams, variants_for_kind
 
 log = logging.getLogger(__name__)
@@ -51,13 +51,23 @@ class FormatVersionMismatch(CuclgenError):
 
 
 def op_signature(node: OpNode, edges) -> str:
-    """``conv:k{k}:s{s}:p{p}:oc{oc}:in{b}x{ic}x{h}x{w}[:relu]`` (tuner.py:66-75)."""
-    if node.kind != KIND_CONV:
-        raise CuclgenError(f"no signature for kind {node.kind}")
-    p = node.params
-    b, ic, h, w = edges[node.inputs[0]].sizes
-    sig = f"conv:k{p.ksz}:s{p.stride}:p{p.pad}:oc{p.out_chans}:in{b}x{ic}x{h}x{w}"
-    return sig + (f":{node.fused_activation}" if node.fused_activation else "")
+    """Canonical per-op key (tuner.py:66-89): ``conv:k{k}:s{s}:p{p}:oc{oc}:in{b}x{ic}x{h}x{w}[:relu]``,
+    ``pool_max:k..:s..:p..:in{b}x{c}x{h}x{w}``, ``relu:in{dims}``, ``xpose:{src}-to-{dst}``."""
+    if node.kind == KIND_CONV:
+        p = node.params
+        b, ic, h, w = edges[node.inputs[0]].sizes
+        sig = f"conv:k{p.ksz}:s{p.stride}:p{p.pad}:oc{p.out_chans}:in{b}x{ic}x{h}x{w}"
+        return sig + (f":{node.fused_activation}" if node.fused_activation else "")
+    if node.kind == KIND_POOL:
+        p = node.params
+        b, c, h, w = edges[node.inputs[0]].sizes
+        return f"pool_max:k{p.ksz}:s{p.stride}:p{p.pad}:in{b}x{c}x{h}x{w}"
+    if node.kind == KIND_ACT:
+        return "relu:in" + "x".join(str(s) for s in edges[node.inputs[0]].sizes)
+    if node.kind == KIND_CONVERT:
+        fmt = lambda s: "_".join(f"{n}{v}" for n, v in zip(s.names, s.sizes))  # noqa: E731
+        return f"xpose:{fmt(edges[node.inputs[0]])}-to-{fmt(edges[node.outputs[0]])}"
+    raise CuclgenError(f"no signature for kind {node.kind}")
 
 
 def conv_flops(p: ConvParams, b: int, ic: int, h: int, w: int) -> int:

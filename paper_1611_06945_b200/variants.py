@@ -20,6 +20,13 @@ launch plan (C descriptor + tune struct) the C ABI executes:
 Every kernel reads canonical NCHW / OIHW and writes NCHW, so
 ``required_formats`` is canonical for all of them (no conversion passes,
 unlike ConvTiled's padded NHWC output, variants.py:416-424).
+
+The non-conv kinds of a whole-network run are variants too,
+each bound to a libb2conv kernel:
+
+    pool_max     window max, -inf padding                    (variants.py:688-741)
+    activation   ReLU                                        (variants.py:744-775)
+    xpose        layout conversion: permute / pad / crop     (variants.py:778-827)
 """
 
 from __future__ import annotations
@@ -28,7 +35,8 @@ from dataclasses import dataclass, field
 
 from . import backend
 from .errors import CuclgenError, Inapplicable
-from .frontend import KIND_CONV, OpNode
+from .frontend import KIND_ACT, KIND_CONV, KIND_CONVERT, KIND_POOL, OpNode
+from .graphopt import VariantFormats
 
 STATIC = "static"
 DYNAMIC = "dynamic"
@@ -104,14 +112,6 @@ class TuneParams:
 
 
 DEFAULT_TUNE = TuneParams()
-
-
-@dataclass(frozen=True)
-class VariantFormats:
-    """Operand layouts a variant requires; empty/None = canonical (graphopt.py:89-94)."""
-
-    inputs: dict = field(default_factory=dict)
-    output: object = None
 
 
 @dataclass(frozen=True)
@@ -286,7 +286,78 @@ class ConvFC(_UmmaFamily):
     name, rank, vid = "conv_fc", 4, backend.VAR_FC
 
 
-VARIANTS: dict = {v.name: v for v in (ConvSimple(), ConvTiled(), ConvUmma(), Conv1x1(), ConvFC())}
+@dataclass(frozen=True)
+class NodePlan:
+    """What ``generate`` returns for a non-conv node: the C descriptor of one
+    pool / ReLU / conversion launch (``desc`` is a PoolDesc, an element count,
+    or an XposeDesc)."""
+
+    variant: str
+    kind: str
+    desc: object
+    params: TuneParams
+
+    @property
+    def name(self) -> str:
+        return f"{self.variant}_{self.kind.lower()}"
+
+
+class _NodeVariant(Variant):
+    """One fixed kernel per node kind; TuneParams are accepted and ignored."""
+
+    rank = 0
+
+    def applies(self, node, edges, params):
+        if node.kind != self.kind:
+            return f"kind {node.kind} != {self.kind}"
+        return self._why_not(node, edges)
+
+    def _why_not(self, node, edges):
+        return None
+
+    def generate(self, node, edges, params=None, mode: str = STATIC) -> NodePlan:
+        reason = self.applies(node, edges, params)
+        if reason:
+            raise Inapplicable(f"{self.name} on '{node.name}': {reason}")
+        return NodePlan(self.name, self.kind, self._desc(node, edges), params or DEFAULT_TUNE)
+
+
+class PoolMax(_NodeVariant):
+    name, kind = "pool_max", KIND_POOL
+
+    def _desc(self, node, edges):
+        i, o = edges[node.inputs[0]], edges[node.outputs[0]]
+        p = node.params
+        return backend.PoolDesc(*(i.size_of(d) for d in ("img", "chan", "y", "x")), p.ksz, p.stride, p.pad,
+                                o.size_of("y"), o.size_of("x"))
+
+
+class Activation(_NodeVariant):
+    name, kind = "activation", KIND_ACT
+
+    def _why_not(self, node, edges):
+        return None if node.params.func == "relu" else f"unknown activation '{node.params.func}'"
+
+    def _desc(self, node, edges):
+        return edges[node.outputs[0]].num_elems
+
+
+class Xpose(_NodeVariant):
+    name, kind = "xpose", KIND_CONVERT
+
+    def _why_not(self, node, edges):
+        src, dst = edges[node.inputs[0]], edges[node.outputs[0]]
+        if set(src.names) != set(dst.names):
+            return f"no conversion from {src.names} to {dst.names}"
+        return None
+
+    def _desc(self, node, edges):
+        src, dst = edges[node.inputs[0]], edges[node.outputs[0]]
+        return backend.xpose_desc(src.names, src.sizes, [src.stride_of(n) for n in src.names], dst.names, dst.sizes)
+
+
+VARIANTS: dict = {v.name: v for v in (ConvSimple(), ConvTiled(), ConvUmma(), Conv1x1(), ConvFC(),
+                                      PoolMax(), Activation(), Xpose())}
 
 
 def variants_for_kind(kind: str) -> list:
