@@ -19,6 +19,7 @@
 #include "k_ffma.cuh"
 #include "k_umma.cuh"
 #include "k_tma.cuh"
+#include "k_fcs.cuh"
 
 using namespace b2c;
 
@@ -144,6 +145,16 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             break;
         case B2C_VAR_UMMA:
             break;
+        case B2C_VAR_FC_STREAM: {
+            if (!(d->r == d->h && d->r == d->w && d->pad == 0 && d->oh == 1 && d->ow == 1)) {
+                why = "filters must cover the whole input with 1x1 output"; return B2C_INAPPLICABLE;
+            }
+            if (d->n > 8) { why = "weight streaming is for batch <= 8 (tensor-core conv_fc beyond)"; return B2C_INAPPLICABLE; }
+            if ((d->c * d->r * d->r) % 4) { why = "ic*h*w % 4 != 0 (16-byte rows)"; return B2C_INAPPLICABLE; }
+            if (t->mnb0 != 4 && t->mnb0 != 8) { why = "warps per block (MNb0) must be 4 or 8"; return B2C_INAPPLICABLE; }
+            if (t->mnt1 != 2 && t->mnt1 != 4) { why = "rows per block (MNt1) must be 2 or 4"; return B2C_INAPPLICABLE; }
+            return B2C_OK;
+        }
         default:
             why = "unknown variant";
             return B2C_BAD_ARGS;
@@ -611,6 +622,22 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.pad = d->pad;
     a.gbar = reinterpret_cast<unsigned long long*>(wsb + p.gbar_off);
     a.flt_early = t->prepared ? 1 : 0;  // b2c_conv_prepare synchronises, so a prepared pack is complete
+    {
+        int period = p.kblocks, valid = g.K - TM_BK * (p.kblocks - 1);  // fc (MODE 1): flat K tail
+        if (mode == 0 || mode == 2) {
+            period = p.cblocks;
+            valid = d->c - TM_BK * (period - 1);
+        } else if (mode == 4) {
+            period = p.cblocks;  // x-window chunks per filter row
+            valid = d->r * 4 - TM_BK * (period - 1);
+        } else if (mode == 3) {
+            valid = 4 * (d->r * d->r - TM_TAPS * (p.kblocks - 1));
+        }
+        a.kb_period = std::max(1, period);
+        a.ksteps_last = std::min(TM_BK / 8, std::max(1, (valid + 7) / 8));
+        static const bool no_skip = std::getenv("B2C_NO_KSKIP") != nullptr;  // A/B experiments
+        if (no_skip) a.ksteps_last = TM_BK / 8;
+    }
     const int grid = p.streamk ? p.sk_grid
                      : cl == 2  ? 2 * std::min(a.units, num_sms() / 2)
                                 : std::min(a.units, occ * num_sms());
@@ -642,6 +669,21 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
             if (rc) return rc;
             dim3 grid((g.M + BM - 1) / BM, (g.OC + BN - 1) / BN);
             fn<<<grid, t->mnb0 * t->mnb1, sm, st>>>(g, x, w, bias, y, t->mnb0, t->mnb1, t->kb);
+            break;
+        }
+        case B2C_VAR_FC_STREAM: {
+            using FcsKernel = void (*)(const float*, const float*, const float*, float*, int, int, int, int);
+            const int nb = d->n <= 1 ? 1 : d->n <= 2 ? 2 : d->n <= 4 ? 4 : 8;
+            const int R = t->mnt1;
+            FcsKernel fn = nullptr;
+#define B2C_FCS(NB_, R_) if (nb == NB_ && R == R_) fn = k_fc_stream<NB_, R_>;
+            B2C_FCS(1, 2) B2C_FCS(2, 2) B2C_FCS(4, 2) B2C_FCS(8, 2)
+            B2C_FCS(1, 4) B2C_FCS(2, 4) B2C_FCS(4, 4) B2C_FCS(8, 4)
+#undef B2C_FCS
+            if (!fn) return fail(B2C_INAPPLICABLE, "no weight-streaming kernel for this shape");
+            const int W = t->mnb0;
+            const size_t sm = (size_t)W * R * nb * sizeof(float);
+            fn<<<(g.OC + R - 1) / R, 32 * W, sm, st>>>(x, w, bias, y, g.N, g.OC, g.K, g.act);
             break;
         }
         default: {

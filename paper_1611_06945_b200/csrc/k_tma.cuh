@@ -103,8 +103,12 @@ struct TmaCfg {
     static constexpr int SM_STAGES = BUDGET / STAGE_BYTES;
     static constexpr int STAGES = SM_STAGES < 8 ? SM_STAGES : 8;
     static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES;
-    static constexpr int A_SLOTS = 2;                        // TMEM A stages (raw | lo: 64 columns each)
     static constexpr int TMEM_COLS = OCC == 2 ? 256 : 512;
+    // TMEM A stages (raw | lo: 64 columns each): as many as the columns left beside the two
+    // accumulators allow (<= 4), so a split is not held up waiting for the MMAs of the stage
+    // two back to release its slot (the 2-slot loop was paced split -> MMA issue -> MMA done).
+    static constexpr int A_SLOTS_FIT = (TMEM_COLS - ACC_COLS) / 64;
+    static constexpr int A_SLOTS = A_SLOTS_FIT < 4 ? A_SLOTS_FIT : 4;
     static_assert(ACC_COLS + A_SLOTS * 64 <= TMEM_COLS, "TMEM budget");
     static constexpr bool SW128 = MODE != 3;
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
@@ -140,6 +144,9 @@ struct TArgs {
     int hp, wp, pad;
     unsigned long long* gbar;  // grid barrier counter (monotonic; zero at allocation)
     int flt_early;      // packed filters are complete: the loader may fetch them before griddepcontrol.wait
+    // K blocks whose index % kb_period == kb_period - 1 hold only ksteps_last valid
+    // groups of 8 K (channel / window / K tail); the MMAs skip the all-zero rest.
+    int kb_period, ksteps_last;
 };
 
 // Walks a CTA's work: units blockIdx, +stride, ... ; or, in stream-K mode, the
@@ -653,8 +660,11 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
         for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
             int kin = 0;
+            int kph = w.kb_begin % a.kb_period;  // position of this K block within its period
             for (int i = 0; i < w.nkb; ++i, ++n) {
                 const int slot = cidx & 1;
+                const int nsteps = (kph == a.kb_period - 1) ? a.ksteps_last : TM_BK / 8;
+                if (++kph == a.kb_period) kph = 0;
                 const bool first = kin == 0;
                 const bool last = (kin == G - 1) || (i == w.nkb - 1);
                 if (first && cidx >= 2) {
@@ -674,6 +684,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
                     const uint32_t d = tmem_base + (uint32_t)(slot * BN);
 #pragma unroll
                     for (int s = 0; s < TM_BK / 8; ++s) {
+                        if (s >= nsteps) break;  // all-zero K tail of the block (exact: 0 * finite)
                         uint64_t dbh, dbl;
                         if (Cfg::SW128) {
                             dbh = umma_desc_sw128(b_raw + s * 32);

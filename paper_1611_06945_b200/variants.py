@@ -286,6 +286,21 @@ class ConvFC(_UmmaFamily):
     name, rank, vid = "conv_fc", 4, backend.VAR_FC
 
 
+class ConvFCStream(Variant):
+    """ConvFC (variants.py:328-373) as an fp32 FFMA weight-streaming kernel for
+    batch <= 8, where the op is HBM-bound: MNb0 = warps per block (4|8), MNt1 =
+    out_chan rows per block (2|4)."""
+
+    name, rank, vid = "conv_fc_stream", 5, backend.VAR_FC_STREAM
+
+    def default_params(self, node, edges):
+        return TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)
+
+    def space(self, node, edges):
+        out = [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=1, vw=1) for wp in (4, 8) for r in (2, 4)]
+        return [p for p in out if self.applies(node, edges, p) is None]
+
+
 @dataclass(frozen=True)
 class NodePlan:
     """What ``generate`` returns for a non-conv node: the C descriptor of one
@@ -356,7 +371,7 @@ class Xpose(_NodeVariant):
         return backend.xpose_desc(src.names, src.sizes, [src.stride_of(n) for n in src.names], dst.names, dst.sizes)
 
 
-VARIANTS: dict = {v.name: v for v in (ConvSimple(), ConvTiled(), ConvUmma(), Conv1x1(), ConvFC(),
+VARIANTS: dict = {v.name: v for v in (ConvSimple(), ConvTiled(), ConvUmma(), Conv1x1(), ConvFC(), ConvFCStream(),
                                       PoolMax(), Activation(), Xpose())}
 
 

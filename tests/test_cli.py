@@ -53,7 +53,7 @@ def test_run_network_with_device_check(cuda, capsys):
     rc = cli.main(["run", "--net", os.path.join(NETS, "googlenet_3a.net"), "--check", "--batch", "2"])
     out = capsys.readouterr().out
     assert rc == cli.EXIT_OK, out
-    assert out.count("sink ") == 4 and "FAIL" not in out and out.count(": pass") == 7
+    assert out.count("sink ") == 4 and "FAIL" not in out and out.count(": pass") == 9
 
 
 @pytest.mark.gpu

@@ -62,6 +62,8 @@ def _variant_params(g):
                     TuneParams(bn=32, swap_ab=True, split_k=2, tma=1, occ=2), TuneParams(bn=64, tma=1, cl=2),
                     TuneParams(bn=96, split_k=2, tma=2, cl=2)):
             out.append((v, prm))
+    out += [("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)),
+            ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1))]
     return [(n, p) for n, p in out if VARIANTS[n].applies(node, g.edges, p) is None]
 
 

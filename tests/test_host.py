@@ -107,8 +107,13 @@ def test_tune_params_string_roundtrip_and_reference_form():
 
 
 def test_variant_rank_order_and_heuristic():
-    assert [v.name for v in variants_for_kind("Convolution")] == ["conv_fc", "conv_1x1", "conv_umma", "conv_tiled", "conv_simple"]
+    assert [v.name for v in variants_for_kind("Convolution")] == ["conv_fc_stream", "conv_fc", "conv_1x1", "conv_umma",
+                                                                  "conv_tiled", "conv_simple"]
     g = g_of(6, 1, 0, 16, (2, 8, 6, 6))
+    assert select_variant(g.node("conv"), g.edges)[0].name == "conv_fc_stream"  # batch <= 8: weight streaming
+    g = g_of(6, 1, 0, 16, (20, 8, 6, 6))
+    assert select_variant(g.node("conv"), g.edges)[0].name == "conv_fc"
+    g = g_of(3, 1, 0, 16, (2, 7, 3, 3))  # ic*h*w = 63: no 16-byte rows
     assert select_variant(g.node("conv"), g.edges)[0].name == "conv_fc"
     g = g_of(1, 1, 0, 16, (2, 8, 6, 6))
     assert select_variant(g.node("conv"), g.edges)[0].name == "conv_1x1"

@@ -143,7 +143,7 @@ def test_plan_graph_networks(fn):
     for name in plan.order:
         kind = plan.graph.node(name).kind
         v = plan.choices[name][0]
-        assert (kind, v) in {("Convolution", "conv_fc"), ("Convolution", "conv_1x1"), ("Convolution", "conv_umma"),
+        assert (kind, v) in {("Convolution", "conv_fc"), ("Convolution", "conv_fc_stream"), ("Convolution", "conv_1x1"), ("Convolution", "conv_umma"),
                              ("Pooling", "pool_max"), ("Activation", "activation")}
 
 

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rows", default=None, help="comma list of corpus rows (default all)")
     ap.add_argument("--merge", default=None, help="existing DB to merge into")
+    ap.add_argument("--nets", default="alexnet,nin,googlenet_3a",
+                    help="also tune the conv nodes of these network files (data/nets) at the same batches")
     args = ap.parse_args()
     db = tuner.load_db(args.merge) if args.merge and os.path.exists(args.merge) else tuner.TuneDB()
     rows = None if args.rows is None else {int(r) for r in args.rows.split(",")}
@@ -45,6 +47,26 @@ def main():
               f"{rec.cost / 1e3:9.2f} us  {op.flops_computed / rec.cost / 1e3:7.1f} TFLOP/s  err={rec.max_rel_err:.2e}  "
               f"({time.time() - t0:.1f}s)", flush=True)
         tuner.save_db(db, args.out)
+    if args.nets and rows is None:
+        from paper_1611_06945_b200 import graphopt
+        from paper_1611_06945_b200.frontend import KIND_CONV, infer_shapes, parse_net
+        from paper_1611_06945_b200.ndarray import DimsSpec
+
+        nets = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1611_06945_b200", "data", "nets")
+        for net in args.nets.split(","):
+            text = open(os.path.join(nets, f"{net}.net")).read()
+            for b in [int(b) for b in args.batches.split(",")]:
+                g = parse_net(text)
+                d = g.edges["data"]
+                g = graphopt.fuse_activations(infer_shapes(g, DimsSpec.row_major(d.names, (b,) + d.sizes[1:])))
+                for node in g.nodes:
+                    if node.kind != KIND_CONV or tuner.op_signature(node, g.edges) in db.records:
+                        continue
+                    rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2)
+                    db.add(rec)
+                    print(f"{net} N={b:2d} {rec.op_signature:42s} {rec.variant:11s} {rec.params.to_string():60s} "
+                          f"{rec.cost / 1e3:9.2f} us", flush=True)
+                tuner.save_db(db, args.out)
     print(f"tuned {len(db.records)} signatures in {time.time() - t_all:.0f}s -> {args.out}")
 
 
