@@ -55,6 +55,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--batches", default="1,5,20")
+    ap.add_argument("--prec", choices=("fp32", "bf16"), default="fp32",
+                    help="fp32: fp32-exact (3xTF32 / FFMA, the headline); bf16: bf16 operands, fp32 accumulate "
+                         "(separately stated tolerance rel 4e-3)")
     ap.add_argument("--db", default=None, help="TuneDB path (default: shipped B200 fp32 DB if present)")
     ap.add_argument("--heuristic", action="store_true", help="ignore the TuneDB, use select_variant's heuristic")
     ap.add_argument("--per-op-out", default=None, help="write per-op CSV here")
@@ -126,7 +129,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_sweep(batches, db, heuristic, rank, world=1, strong=False):
+def build_sweep(batches, db, heuristic, rank, world=1, strong=False, prec=0):
     """(row, BenchOp, node, edges, variant, params) for every op of the sweep.
     Weak scaling: every rank runs every op on its own N images.  Strong
     scaling: rank r takes its contiguous slab of each op's N images
@@ -146,6 +149,14 @@ def build_sweep(batches, db, heuristic, rank, world=1, strong=False):
         g = with_fused(op.graph(), "conv", "relu")
         node = g.node("conv")
         v, params = select_variant(node, g.edges, None if heuristic else db)
+        if prec and params.prec != prec:  # bf16 mode: a record of this precision, else the first bf16 candidate
+            from dataclasses import replace
+
+            from paper_1611_06945_b200 import tuner
+
+            params = replace(params, prec=prec)
+            if v.applies(node, g.edges, params) is not None:
+                v, params = tuner.candidates(node, g.edges, prec=prec)[0]
         out.append((row, op, node, g.edges, v, params))
     return out
 
@@ -208,7 +219,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(c["seconds"] for c in vals), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "global_batch": "1,5,20", "parallelism": "host cores",
+            "config": {"workload": WORKLOAD if not prec else WORKLOAD.replace(", fp32", ", bf16 operands / fp32 accumulate"), "global_batch": "1,5,20", "parallelism": "host cores",
                        "sample": cb["sample"]},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cb["cores"], "kind": "port",
                              "sample": cb["sample"]},
@@ -231,9 +242,10 @@ def run_ours(args, rank, world, local_rank):
         from paper_1611_06945_b200 import backend as _bk
         _bk.lib().b2c_debug_trace_enable(args.debug_flags & ~1)  # never the (CTA-0 trace) bit
     batches = [int(b) for b in args.batches.split(",")]
-    db_path = args.db or tuner.shipped_db_path()
+    prec = 1 if args.prec == "bf16" else 0
+    db_path = args.db or tuner.shipped_db_path(args.prec)
     db = tuner.load_db(db_path) if (os.path.exists(db_path) and not args.heuristic) else None
-    sweep = build_sweep(batches, db, args.heuristic, rank, world, args.strong)
+    sweep = build_sweep(batches, db, args.heuristic, rank, world, args.strong, prec)
 
     ops, hosts, rows = [], [], []
     for row, op, node, edges, v, params in sweep:
@@ -364,7 +376,8 @@ def run_ours(args, rank, world, local_rank):
     dom = max(range(n), key=lambda i: per_op[i])
     d = ops[dom]
     fl, by, t_ms = conv_flops(d.plan.desc), conv_bytes(d.plan.desc), per_op[dom]
-    mode_peak = peaks["bf16_tflops"] / 2 / 3  # 3xTF32: TF32 = bf16/2, three MMA passes
+    # 3xTF32: TF32 = bf16/2, three MMA passes; bf16 mode: one kind::f16 pass
+    mode_peak = peaks["bf16_tflops"] if prec else peaks["bf16_tflops"] / 2 / 3
     ridge = mode_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
     tensor_bound = fl / by >= ridge
     if tensor_bound:
@@ -372,7 +385,8 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(achieved / peaks["bf16_tflops"], 4),
                 "mode_peak": round(mode_peak, 1), "frac_of_mode_peak": round(achieved / mode_peak, 4),
-                "mode_peak_note": "fp32-exact 3xTF32 ceiling = measured bf16 dense / 2 (TF32 rate) / 3 (passes)"}
+                "mode_peak_note": ("bf16 mode: measured bf16 dense peak" if prec else
+                                   "fp32-exact 3xTF32 ceiling = measured bf16 dense / 2 (TF32 rate) / 3 (passes)")}
     else:
         achieved = by / (t_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -407,8 +421,8 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong" if (args.strong and world > 1) else "weak",
-        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": WORKLOAD,
+        "vs_baseline": None, "dtype": args.prec, "data": "synthetic",
+        "config": {"workload": WORKLOAD if not prec else WORKLOAD.replace(", fp32", ", bf16 operands / fp32 accumulate"),
                    "global_batch": ",".join(str(b if args.strong else b * world) for b in batches),
                    "sharding": "batch slabs per op (strong)" if args.strong else "N images per rank (weak)",
                    "output_gather": "NCCL all_gather of every op's slabs, inside the timed step" if gather else "none",

@@ -60,7 +60,7 @@ int check_desc(const b2c_conv_desc* d) {
     const long long wk = (long long)d->k * d->c * d->r * d->r;
     if (xin >= (1ll << 31) || yout >= (1ll << 31) || wk >= (1ll << 31))
         return fail(B2C_UNSUPPORTED, "tensor exceeds 2^31 elements");
-    if (d->prec != B2C_PREC_FP32) return fail(B2C_UNSUPPORTED, "only prec=fp32 is built in this library");
+    if (d->prec != B2C_PREC_FP32 && d->prec != B2C_PREC_BF16) return fail(B2C_BAD_ARGS, "prec must be 0 (fp32) or 1 (bf16)");
     return B2C_OK;
 }
 
@@ -114,6 +114,19 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (rc) { why = g_last_error; return rc; }
     if (!t) { why = "null tune"; return B2C_BAD_ARGS; }
     const long long M = (long long)d->n * d->oh * d->ow;
+    if (d->prec == B2C_PREC_BF16) {
+        // bf16 operands / fp32 accumulate: only the TMA tcgen05 kernel with pixels on M
+        if (t->variant != B2C_VAR_UMMA && t->variant != B2C_VAR_1X1) {
+            why = "bf16 mode: tcgen05 conv_umma / conv_1x1 only"; return B2C_INAPPLICABLE;
+        }
+        if (!t->tma || t->swap_ab || t->cluster == 2 || t->stages == 2 || (t->tma == 2 && d->c <= 4)) {
+            why = "bf16 mode: TMA kernel (tma=1|2), swap_ab=0, single CTAs, not the 8-tap first-layer path";
+            return B2C_INAPPLICABLE;
+        }
+        if (t->tile_n != 32 && t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) {
+            why = "bf16 mode: tile_n in {32, 64, 128, 192}"; return B2C_INAPPLICABLE;
+        }
+    }
     switch (t->variant) {
         case B2C_VAR_SIMPLE:
             return B2C_OK;
@@ -236,8 +249,9 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.kps = (p.kblocks + want - 1) / want;
     p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
     // packed filters: raw | lo per K block; raw only when the TMA kernel takes them as its TMEM A operand
-    p.parts = (p.tma && t->swap_ab) ? 1 : 2;
-    p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * p.parts * p.flt_rows * UMMA_BK * sizeof(float);
+    p.parts = (p.tma && t->swap_ab) || d->prec == B2C_PREC_BF16 ? 1 : 2;
+    const size_t row_bytes = d->prec == B2C_PREC_BF16 ? UMMA_BK * 2 : UMMA_BK * sizeof(float);  // per K block
+    p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * p.parts * p.flt_rows * row_bytes;
     p.streamk = (t->tma && t->split_k == 0) ? 1 : 0;
     p.sk_grid = p.sk_maxc = 0;
     size_t nslots = p.split > 1 ? (size_t)p.tiles * p.split : 0;
@@ -303,6 +317,13 @@ int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* w
     if (p.wpk_bytes == 0) return B2C_OK;  // TMA fc path reads raw filters
     if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
     const Geom g = make_geom(d);
+    if (d->prec == B2C_PREC_BF16) {
+        const long long total = (long long)p.wpk_bytes / 2;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+        k_pack_filters_bf16<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<uint16_t*>(ws), p.flt_rows, p.kblocks,
+                                                    FastDiv((uint32_t)p.cblocks), p.kmode, total);
+        return B2C_OK;
+    }
     const long long total = (long long)p.wpk_bytes / 4;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
     k_pack_filters<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<float*>(ws), p.flt_rows, p.kblocks,
@@ -467,10 +488,21 @@ struct TconvEntry {
     int threads;
 };
 
-template <int BN, bool SWAP, int MODE, int OCC, int CL>
+template <int BN, bool SWAP, int MODE, int OCC, int CL, int PREC = 0>
 TconvEntry tconv_entry() {
-    using C = TmaCfg<BN, SWAP, MODE, OCC, CL>;
-    return TconvEntry{&k_tconv<BN, SWAP, MODE, OCC, CL>, C::SMEM, C::THREADS};
+    using C = TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>;
+    return TconvEntry{&k_tconv<BN, SWAP, MODE, OCC, CL, PREC>, C::SMEM, C::THREADS};
+}
+
+template <int MODE>
+TconvEntry tconv_pick_bf16(int bn) {
+    switch (bn) {
+        case 32: return tconv_entry<32, false, MODE, 1, 1, 1>();
+        case 64: return tconv_entry<64, false, MODE, 1, 1, 1>();
+        case 128: return tconv_entry<128, false, MODE, 1, 1, 1>();
+        case 192: return tconv_entry<192, false, MODE, 1, 1, 1>();
+    }
+    return TconvEntry{nullptr, 0, 0};
 }
 
 template <bool SWAP, int MODE>
@@ -538,7 +570,12 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     const int mode = p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
     const int cl = t->cluster == 2 ? 2 : 1;
-    TconvEntry e = tconv_pick(t->tile_n, t->swap_ab, mode, occ, cl);
+    TconvEntry e{nullptr, 0, 0};
+    if (d->prec == B2C_PREC_BF16)
+        e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
+            : mode == 4 ? tconv_pick_bf16<4>(t->tile_n) : TconvEntry{nullptr, 0, 0};
+    else
+        e = tconv_pick(t->tile_n, t->swap_ab, mode, occ, cl);
     if (!e.fn) return fail(B2C_INAPPLICABLE, "no TMA tcgen05 kernel for this tile");
     rc = ensure_smem_attr((const void*)e.fn, e.smem);
     if (rc) return rc;

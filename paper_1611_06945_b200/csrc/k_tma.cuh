@@ -72,8 +72,13 @@ constexpr int TM_HDR = 2048;           // barriers, TMEM slot, flags (< 1 KB); u
 constexpr int TM_MAX_SMEM = 232448;    // 227 KB opt-in per CTA
 constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 
-template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1>
+// PREC 0: fp32-exact 3xTF32 (kind::tf32, A = raw | lo in TMEM, B = packed raw | lo).
+// PREC 1: bf16 operands, fp32 accumulate (kind::f16): the split warps round the fp32
+//         pixel tile to bf16 into TMEM; filters are packed once as bf16 in the
+//         no-swizzle core-matrix layout [8-element chunk][rows][16 B].
+template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
+    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && CL == 1), "bf16: pixels on M, packed filters");
     static_assert(CL == 1 || (CL == 2 && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
@@ -92,11 +97,11 @@ struct TmaCfg {
     static constexpr bool A_PRESPLIT = false;
     static constexpr bool B_SPLIT = SWAP || MODE == 1;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
-    static constexpr int B_BYTES = 2 * BN * 128;  // raw + lo
+    static constexpr int B_BYTES = PREC ? BN * 64 : 2 * BN * 128;  // bf16 | raw + lo
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
     static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
-    static constexpr int FLT_STAGE = (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block (raw [| lo])
+    static constexpr int FLT_STAGE = PREC ? FLT_ROWS * 64 : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
     static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
     // OCC CTAs per SM share its 228 KB of shared memory (1 KB per CTA is the driver's) and 512 TMEM columns
     static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024;
@@ -429,6 +434,22 @@ __device__ __forceinline__ void a_to_tmem(uint32_t a, int tid, uint32_t tcol) {
     tmem_st32(tcol + 32, l);
 }
 
+// bf16 mode: the same 32 fp32 of this thread's row, rounded to bf16 and packed in
+// pairs (even K in the low half) into 16 TMEM columns.
+template <bool SW128>
+__device__ __forceinline__ void a_to_tmem_bf16(uint32_t a, int tid, uint32_t tcol) {
+    uint32_t r[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t off = SW128 ? (uint32_t)tid * 128u + (uint32_t)((c ^ (tid & 7)) * 16)
+                                   : (uint32_t)(c * TM_M * 16 + tid * 16);
+        const float4 q = lds128(a + off);
+        r[2 * c] = pack_bf16x2(q.x, q.y);
+        r[2 * c + 1] = pack_bf16x2(q.z, q.w);
+    }
+    tmem_st16u(tcol, r);
+}
+
 // One unit's output: + bias, ReLU (variants.py:160-165), NCHW stores; with
 // split-K, the fp32 partial goes to the workspace and the unit that arrives
 // last for its tile (atomic ticket) reduces all partials in split order, so
@@ -531,10 +552,10 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
 
 // ----------------------------------------------------------------------------- main kernel
 
-template <int BN, bool SWAP, int MODE, int OCC, int CL>
-__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
+template <int BN, bool SWAP, int MODE, int OCC, int CL, int PREC = 0>
+__global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS, OCC)
     k_tconv(const __grid_constant__ CUtensorMap tm_pix, const __grid_constant__ CUtensorMap tm_flt, TArgs a) {
-    using Cfg = TmaCfg<BN, SWAP, MODE, OCC, CL>;
+    using Cfg = TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>;
     constexpr int STAGES = Cfg::STAGES;
     constexpr int DC = Cfg::DRAIN_COLS;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -606,7 +627,10 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
                     mbar_wait(smem_u32(&afree_bar[aslot]), (uint32_t)((n / Cfg::A_SLOTS) - 1) & 1u);
                 tc_fence_after();
                 const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + aslot * 64);
-                if (!(a.trace & 8)) a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);  // debug bit 3: skip
+                if (PREC == 1)
+                    a_to_tmem_bf16<Cfg::SW128>(sbase, tid, t_lane + acol);
+                else if (!(a.trace & 8))
+                    a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);  // debug bit 3: skip
                 if (Cfg::B_SPLIT && !(a.trace & 4)) split_tile<BN>(sbase + Cfg::A_SMEM, tid);
                 fence_proxy_async_smem();
                 tmem_st_wait();
@@ -654,7 +678,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
         if (dtid == 0) B2C_TRACE(a.trace, 6);
     } else if (warp == Cfg::MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer (whole warp waits, one lane issues)
-        constexpr uint32_t idesc = umma_idesc(2, TM_M, BN);
+        constexpr uint32_t idesc = umma_idesc(PREC == 1 ? 1 : 2, TM_M, BN);
         int stage = 0, cidx = 0, n = 0;
         uint32_t phase = 0;
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
@@ -682,6 +706,14 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
                     const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
                     const uint32_t b_lo = b_raw + BN * 128;
                     const uint32_t d = tmem_base + (uint32_t)(slot * BN);
+                    if constexpr (PREC == 1) {  // bf16: two K=16 MMAs per 32-wide K block
+#pragma unroll
+                        for (int s = 0; s < TM_BK / 16; ++s) {
+                            if (2 * s >= nsteps) break;
+                            const uint64_t db = umma_desc(b_raw + s * 2 * BN * 16, BN * 16, 128);
+                            mma_bf16_ts(d, a_hi + 8 * s, db, idesc, (first && s == 0) ? 0u : 1u);
+                        }
+                    } else {
 #pragma unroll
                     for (int s = 0; s < TM_BK / 8; ++s) {
                         if (s >= nsteps) break;  // all-zero K tail of the block (exact: 0 * finite)
@@ -698,6 +730,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL>::THREADS, OCC)
                             mma_tf32_ts(d, a_hi + 8 * s, dbl, idesc, 1u);
                             mma_tf32_ts(d, a_lo + 8 * s, dbh, idesc, 1u);
                         }
+                    }
                     }
                     if (CL == 2)  // the stage's filter half may be refilled by either CTA
                         tc_commit_mc(smem_u32(&empty_bar[stage]), (uint16_t)0x3);

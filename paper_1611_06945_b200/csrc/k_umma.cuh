@@ -50,6 +50,7 @@
 // ReLU, NCHW stores.  Split-K CTAs write partials to workspace; the last CTA
 // of a tile (atomic ticket) reduces them in split order (deterministic).
 #pragma once
+#include <cuda_bf16.h>
 #include "common.cuh"
 
 namespace b2c {
@@ -234,6 +235,53 @@ __device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* acc) {
 // chunks XOR-swizzled by row % 8 (the SWIZZLE_128B image k_tconv reads).
 // parts == 1 packs the raw half only (k_tconv computes lo itself when the
 // filter tile is its TMEM A operand).
+// Filter value at K position kk (0..31) of K block kb for out_chan oc, in the
+// K order of `kmode` (see kmode_for in b2conv.cu); 0 past the real K.
+__device__ __forceinline__ float packed_k_value(const Geom& g, const float* __restrict__ w, int oc, int kb, int kk,
+                                                FastDiv fCB, int kmode) {
+    if (oc >= g.OC) return 0.0f;
+    if (kmode == 3) {
+        uint32_t tap, cb, ky, kx;
+        fCB.divmod((uint32_t)kb, tap, cb);
+        g.fR.divmod(tap, ky, kx);
+        const int ic = (int)cb * UMMA_BK + kk;
+        return ic < g.C ? w[(long long)oc * g.K + ((long long)ic * g.R + ky) * g.R + kx] : 0.0f;
+    }
+    if (kmode == 5) {
+        uint32_t ky, kc;
+        fCB.divmod((uint32_t)kb, ky, kc);
+        const int wi = (int)kc * 32 + kk;
+        const int kx = wi >> 2, ch = wi & 3;
+        return (kx < g.R && ch < g.C) ? w[(long long)oc * g.K + ((long long)ch * g.R + ky) * g.R + kx] : 0.0f;
+    }
+    if (kmode == 4) {
+        const int tap = kb * 8 + (kk >> 2), ch = kk & 3;
+        return (tap < g.RR && ch < g.C) ? w[(long long)oc * g.K + (long long)ch * g.RR + tap] : 0.0f;
+    }
+    const int k = kb * UMMA_BK + kk;
+    return k < g.K ? w[(long long)oc * g.K + k] : 0.0f;
+}
+
+// bf16 pack for the TMA kernel's bf16 mode: [filter tile][K block][8-element chunk 0..3][rows][8 x bf16]
+// (UMMA no-swizzle K-major core matrices: 8 rows x 16 B contiguous), round to nearest even.
+__global__ void __launch_bounds__(256) k_pack_filters_bf16(Geom g, const float* __restrict__ w,
+                                                           uint16_t* __restrict__ out, int rows, int kblocks,
+                                                           FastDiv fCB, int kmode, long long total) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)(i & 7);
+        long long t = i >> 3;
+        const int r = (int)(t % rows);
+        t /= rows;
+        const int c = (int)(t & 3);
+        t >>= 2;
+        const int kb = (int)(t % kblocks);
+        const int tile = (int)(t / kblocks);
+        const float v = packed_k_value(g, w, tile * rows + r, kb, 8 * c + e, fCB, kmode);
+        out[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __restrict__ w, float* __restrict__ out,
                                                       int rows, int kblocks, FastDiv fCB, int kmode,
                                                       long long total, int swz, int parts) {

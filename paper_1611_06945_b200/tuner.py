@@ -81,8 +81,14 @@ class ToleranceSpec:
     abs_floor: float = 1e-6
 
 
-def tolerance_for(reduction_terms: int) -> ToleranceSpec:
-    """rel 1e-5 up to 4096 reduction terms, 1e-3 beyond (oracle.py:31-38)."""
+BF16_REL_TOL = 4e-3  # bf16 operands, fp32 accumulate
+
+
+def tolerance_for(reduction_terms: int, prec: int = 0) -> ToleranceSpec:
+    """rel 1e-5 up to 4096 reduction terms, 1e-3 beyond (oracle.py:31-38); the
+    separately stated bf16-mode tolerance is rel 4e-3."""
+    if prec == 1:
+        return ToleranceSpec(rel_tol=BF16_REL_TOL)
     return ToleranceSpec(rel_tol=1e-3) if reduction_terms > LONG_REDUCTION_TERMS else ToleranceSpec()
 
 
@@ -182,19 +188,25 @@ def load_db(path) -> TuneDB:
     return db
 
 
-def candidates(node: OpNode, edges, space: TuneSpace | None = None) -> list:
-    """All applicable (variant, params), most specialized variant first (tuner.py:301-308)."""
+def candidates(node: OpNode, edges, space: TuneSpace | None = None, prec: int = 0) -> list:
+    """All applicable (variant, params), most specialized variant first (tuner.py:301-308).
+    ``prec`` 1 re-targets every candidate to the bf16 mode (TuneParams.prec) and keeps
+    the applicable ones."""
+    from .variants import with_prec
+
     space = space or default_space()
     out = []
     for v in variants_for_kind(node.kind):
         plist = space.per_variant.get(v.name)
-        plist = v.space(node, edges) if plist is None else v.tune_candidates(node, edges, plist)
-        out.extend((v, p) for p in plist)
+        plist = v.space(node, edges) if plist is None else list(plist)
+        if prec:
+            plist = with_prec(plist, prec)
+        out.extend((v, p) for p in v.tune_candidates(node, edges, plist))
     return out
 
 
 def sweep(node: OpNode, edges, space: TuneSpace | None = None, objective: str = WALL, reps: int = 5,
-          warmup: int = 2, l2_flush: bool = True, seed: str = "validate", jobs: int = 1) -> TuneRecord:
+          warmup: int = 2, l2_flush: bool = True, seed: str = "validate", jobs: int = 1, prec: int = 0) -> TuneRecord:
     """Time every applicable candidate on the device and return the fastest one
     that matches the exact-order conv_simple output within tolerance.  Ties
     break by enumeration order (specialized variants first), tuner.py:367-373."""
@@ -202,7 +214,7 @@ def sweep(node: OpNode, edges, space: TuneSpace | None = None, objective: str = 
         raise CuclgenError("objective 'model' is the simulator's counter model; the B200 tuner times on device ('wall')")
     if node.kind != KIND_CONV:
         raise AllCandidatesFailed(f"no variant applies to '{node.name}'")
-    cands = candidates(node, edges, space)
+    cands = candidates(node, edges, space, prec)
     if not cands:
         raise AllCandidatesFailed(f"no variant applies to '{node.name}'")
     import torch
@@ -215,7 +227,7 @@ def sweep(node: OpNode, edges, space: TuneSpace | None = None, objective: str = 
     ref = ConvOp(ref_plan, x, w, b)
     ref.launch()
     torch.cuda.synchronize()
-    tol = tolerance_for(edges[node.inputs[0]].size_of("chan") * node.params.ksz ** 2)
+    tol = tolerance_for(edges[node.inputs[0]].size_of("chan") * node.params.ksz ** 2, prec)
     sig = op_signature(node, edges)
     best, best_key, failures = None, None, []
     for idx, (v, params) in enumerate(cands):

@@ -64,6 +64,7 @@ class TuneParams:
     tma: int = 0  # tcgen05: 1 = TMA-fed kernel (im2col on an NHWC copy / 2-D tiles), 2 = 2-D tiles for 1x1; 0 = warp gathers
     occ: int = 1  # TMA kernel: CTAs per SM (2 needs bn <= 64)
     cl: int = 1  # TMA kernel: 2 = CTA pairs sharing (multicasting) the filter stages
+    prec: int = 0  # 0 fp32-exact (default), 1 bf16 operands / fp32 accumulate (TMA tcgen05 kernel only)
 
     def __post_init__(self):
         if min(self.mnt) < 1 or min(self.mnb) < 1 or self.kb < 1:
@@ -85,7 +86,8 @@ class TuneParams:
         return (f"MNt={self.mnt[0]}:{self.mnt[1]},MNb={self.mnb[0]}:{self.mnb[1]},Kb={self.kb},vw={self.vw},"
                 f"lf={int(self.use_local_filts)},li={int(self.use_local_in)},"
                 f"BN={self.bn},sk={self.split_k},sw={int(self.swap_ab)},dr={self.drain}"
-                + (f",tm={int(self.tma)}" if self.tma else "") + (f",oc={self.occ}" if self.occ != 1 else "") + (f",cl={self.cl}" if self.cl != 1 else ""))
+                + (f",tm={int(self.tma)}" if self.tma else "") + (f",oc={self.occ}" if self.occ != 1 else "") + (f",cl={self.cl}" if self.cl != 1 else "")
+                + (f",pr={self.prec}" if self.prec else ""))
 
     @staticmethod
     def from_string(text: str) -> "TuneParams":
@@ -106,6 +108,7 @@ class TuneParams:
                 tma=int(kv.get("tm", "0")),
                 occ=int(kv.get("oc", "1")),
                 cl=int(kv.get("cl", "1")),
+                prec=int(kv.get("pr", "0")),
             )
         except (KeyError, ValueError) as e:
             raise CuclgenError(f"bad tune-params string {text!r}: {e}") from None
@@ -186,7 +189,7 @@ class Variant:
             return f"kind {node.kind} != {self.kind}"
         if node.fused_activation not in (None, "relu"):
             return f"no fused form for activation '{node.fused_activation}'"
-        return backend.applies(conv_desc(node, edges), self.tune_struct(params))
+        return backend.applies(conv_desc(node, edges, params.prec), self.tune_struct(params))
 
     def required_formats(self, node: OpNode, edges, params: TuneParams) -> VariantFormats:
         return VariantFormats()
@@ -205,7 +208,7 @@ class Variant:
         reason = self.applies(node, edges, params)
         if reason:
             raise Inapplicable(f"{self.name} on '{node.name}': {reason}")
-        return KernelPlan(self.name, conv_desc(node, edges), self.tune_struct(params), params)
+        return KernelPlan(self.name, conv_desc(node, edges, params.prec), self.tune_struct(params), params)
 
 
 class ConvSimple(Variant):
@@ -272,6 +275,13 @@ class _UmmaFamily(Variant):
                     for tma in ((1, 2) if split == 0 else (1, 2, 0)):
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
         return [p for p in out if self.applies(node, edges, p) is None]
+
+
+def with_prec(params_list, prec: int) -> list:
+    """The same candidates in another precision mode (TuneParams.prec)."""
+    from dataclasses import replace
+
+    return [replace(p, prec=prec) for p in params_list]
 
 
 class ConvUmma(_UmmaFamily):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rows", default=None, help="comma list of corpus rows (default all)")
     ap.add_argument("--merge", default=None, help="existing DB to merge into")
+    ap.add_argument("--prec", type=int, default=0, help="0 fp32-exact, 1 bf16 mode")
     ap.add_argument("--nets", default="alexnet,nin,googlenet_3a",
                     help="also tune the conv nodes of these network files (data/nets) at the same batches")
     args = ap.parse_args()
@@ -41,7 +42,7 @@ def main():
         g = with_fused(op.graph(), "conv", "relu")
         node = g.node("conv")
         t0 = time.time()
-        rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2)
+        rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2, prec=args.prec)
         db.add(rec)
         print(f"row{row:02d} N={op.batch:2d} {rec.op_signature:42s} {rec.variant:11s} {rec.params.to_string():60s} "
               f"{rec.cost / 1e3:9.2f} us  {op.flops_computed / rec.cost / 1e3:7.1f} TFLOP/s  err={rec.max_rel_err:.2e}  "
@@ -62,7 +63,7 @@ def main():
                 for node in g.nodes:
                     if node.kind != KIND_CONV or tuner.op_signature(node, g.edges) in db.records:
                         continue
-                    rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2)
+                    rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2, prec=args.prec)
                     db.add(rec)
                     print(f"{net} N={b:2d} {rec.op_signature:42s} {rec.variant:11s} {rec.params.to_string():60s} "
                           f"{rec.cost / 1e3:9.2f} us", flush=True)
