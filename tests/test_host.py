@@ -212,3 +212,21 @@ def test_model_objective_rejected():
 
 def test_tolerance_rule():
     assert tuner.tolerance_for(4096).rel_tol == 1e-5 and tuner.tolerance_for(4097).rel_tol == 1e-3
+
+
+def test_bf16_mode_params_and_applicability():
+    """bf16 mode (TuneParams.prec = 1, key ``pr``): TMA tcgen05 kernel with pixels on M only."""
+    p = TuneParams.from_string("MNt=4:4,MNb=16:16,Kb=4,vw=4,lf=1,li=1,BN=64,sk=1,sw=0,dr=0,tm=1,pr=1")
+    assert p.prec == 1 and p.to_string().endswith(",pr=1") and TuneParams.from_string(p.to_string()) == p
+    assert TuneParams().to_string().count("pr=") == 0
+    g = g_of(3, 1, 1, 64, (2, 32, 13, 13))
+    node = g.node("conv")
+    assert VARIANTS["conv_umma"].applies(node, g.edges, p) is None
+    assert VARIANTS["conv_umma"].generate(node, g.edges, p).desc.prec == 1
+    for bad in (TuneParams(bn=64, prec=1), TuneParams(bn=64, tma=1, swap_ab=True, prec=1),
+                TuneParams(bn=96, tma=1, prec=1), TuneParams(bn=64, tma=1, occ=2, prec=1)):
+        assert VARIANTS["conv_umma"].applies(node, g.edges, bad) is not None, bad
+    assert VARIANTS["conv_simple"].applies(node, g.edges, TuneParams(prec=1)) is not None
+    cands = tuner.candidates(node, g.edges, prec=1)
+    assert cands and all(p.prec == 1 and v.name in ("conv_umma", "conv_1x1") for v, p in cands)
+    assert tuner.tolerance_for(9999, prec=1).rel_tol == 4e-3 and tuner.tolerance_for(100).rel_tol == 1e-5
