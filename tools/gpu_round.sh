@@ -18,6 +18,9 @@ ROW=$(python -c "import json;d=json.load(open('$OUT/bench.json'));print(d['roofl
 BATCH=$(python -c "import json;d=json.load(open('$OUT/bench.json'));print(d['roofline']['op'].split(':in')[1].split('x')[0])")
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_(umma|tconv|tiled|simple|fc)" -s 2 -c 1 -o $OUT/prof_dom \
    python tools/run_op.py --row $ROW --batch $BATCH --reps 3 > $OUT/ncu_full.log 2>&1
+if [ "$ROW" != "42" ] || [ "$BATCH" != "20" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_tconv" -s 2 -c 1 -o $OUT/prof_r42 \
    python tools/run_op.py --row 42 --batch 20 --reps 3 > $OUT/ncu_full42.log 2>&1
+fi
+du -sh $OUT/*
 echo done
