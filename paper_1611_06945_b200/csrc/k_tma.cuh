@@ -79,6 +79,7 @@ constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
     static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && CL == 1), "bf16: pixels on M, packed filters");
+    static_assert(MODE != 5 || CL == 1, "MODE 5: single CTAs");
     static_assert(CL == 1 || (CL == 2 && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
@@ -118,6 +119,7 @@ struct TmaCfg {
     static constexpr bool SW128 = MODE != 3;
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
     static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
+    static_assert(MODE != 5 || !SWAP, "MODE 5 tiles are pixel runs on M (split warps transpose them)");
     static_assert(STAGES >= 2, "need at least two stages");
     static_assert(DRAIN_COLS % 8 == 0, "TMEM drain granularity");
 };
@@ -197,7 +199,7 @@ __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     w.n0 = nt * FLT_ROWS;
     w.kb_begin = w.z * a.kps;
     w.nkb = min(a.kblocks, w.kb_begin + a.kps) - w.kb_begin;
-    if (MODE == 4) {
+    if (MODE == 4 || MODE == 5) {  // MODE 5: tiles_y = by = 1, bx = 128 (pixel runs of one image)
         const int per_img = a.tiles_x * a.tiles_y;
         w.b = mt / per_img;
         const int r = mt - w.b * per_img;
@@ -450,6 +452,32 @@ __device__ __forceinline__ void a_to_tmem_bf16(uint32_t a, int tid, uint32_t tco
     tmem_st16u(tcol, r);
 }
 
+// MODE 5 (1x1 convs read straight from NCHW): the TMA box is [32 channels][128
+// pixels] (no swizzle), so thread tid's row is a column of it: 32 scalar smem
+// loads at a 512-byte stride (consecutive threads hit consecutive banks).  PREC 0
+// stores raw | lo (3xTF32), PREC 1 packs bf16 pairs.
+template <int PREC>
+__device__ __forceinline__ void a_to_tmem_cmajor(uint32_t a, int tid, uint32_t tcol) {
+    float v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = lds32(a + (uint32_t)(c * TM_M + tid) * 4u);
+    if constexpr (PREC == 1) {
+        uint32_t r[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+        tmem_st16u(tcol, r);
+    } else {
+        float l[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float h;
+            split_tf32(v[j], h, l[j]);
+        }
+        tmem_st32(tcol, v);
+        tmem_st32(tcol + 32, l);
+    }
+}
+
 // One unit's output: + bias, ReLU (variants.py:160-165), NCHW stores; with
 // split-K, the fp32 partial goes to the workspace and the unit that arrives
 // last for its tile (atomic ticket) reduces all partials in split order, so
@@ -491,7 +519,11 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
     float* __restrict__ yp = a.y;
     if (!SWAP) {  // row = output pixel, columns = out_chans
         long long row_out;
-        if (MODE == 4) {  // rectangular tile: row = y * bx + x
+        if (MODE == 5) {  // run of 128 pixels of image b starting at ox0
+            const int p = w.ox0 + row;
+            if (p >= g.PQ) return;
+            row_out = (long long)w.b * g.OC * g.PQ + p;
+        } else if (MODE == 4) {  // rectangular tile: row = y * bx + x
             const int y = row / a.bx, x = row - (row / a.bx) * a.bx;
             const int oy = w.oy0 + y, ox = w.ox0 + x;
             if (y >= a.by || oy >= g.OH || ox >= g.OW) return;
@@ -627,7 +659,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     mbar_wait(smem_u32(&afree_bar[aslot]), (uint32_t)((n / Cfg::A_SLOTS) - 1) & 1u);
                 tc_fence_after();
                 const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + aslot * 64);
-                if (PREC == 1)
+                if (MODE == 5)  // channel-major box [32 ch][128 px]: this thread's pixel is column tid
+                    a_to_tmem_cmajor<PREC>(sbase, tid, t_lane + acol);
+                else if (PREC == 1)
                     a_to_tmem_bf16<Cfg::SW128>(sbase, tid, t_lane + acol);
                 else if (!(a.trace & 8))
                     a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);  // debug bit 3: skip
@@ -807,6 +841,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 } else {
                     if (MODE == 2) {
                         tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
+                    } else if (MODE == 5) {  // (pixel run, channel block, image) straight from NCHW x
+                        tma_load_3d(pix, &tm_pix, bar, w.ox0, kb * TM_BK, w.b);
                     } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
                         uint32_t ky, kc;
                         a.fCB.divmod((uint32_t)kb, ky, kc);

@@ -272,7 +272,7 @@ class _UmmaFamily(Variant):
                 for split in (1, 2, 4, 8, 16, 32, 0):  # 0 = stream-K (TMA kernel)
                     if split > 1 and kblocks // split < 2:
                         continue
-                    for tma in ((1, 2) if split == 0 else (1, 2, 0)):
+                    for tma in ((1, 2, 3) if split == 0 else (1, 2, 3, 0)):
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
         return [p for p in out if self.applies(node, edges, p) is None]
 

@@ -38,7 +38,8 @@ def _params():
 
     return [TuneParams(bn=32, tma=1, prec=1), TuneParams(bn=64, split_k=2, tma=1, prec=1),
             TuneParams(bn=128, tma=2, prec=1), TuneParams(bn=192, split_k=0, tma=1, prec=1),
-            TuneParams(bn=64, split_k=0, tma=2, prec=1)]
+            TuneParams(bn=64, split_k=0, tma=2, prec=1), TuneParams(bn=64, tma=3, prec=1),
+            TuneParams(bn=128, split_k=2, tma=3, prec=1)]
 
 
 def _graph(c, relu):
