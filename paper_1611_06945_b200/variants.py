@@ -274,6 +274,10 @@ class _UmmaFamily(Variant):
                         continue
                     for tma in ((1, 2, 3) if split == 0 else (1, 2, 3, 0)):
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
+                        if tma and split and bn <= 64:  # two CTAs per SM
+                            out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))
+                        if tma in (1, 2) and split and bn >= 64 and not swap:  # CTA pairs multicasting filters
+                            out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
         return [p for p in out if self.applies(node, edges, p) is None]
 
 
