@@ -511,7 +511,23 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
         const float* base = a.ws + (size_t)w.pslot0 * BN * TM_M;
 #pragma unroll
         for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
-        for (int zz = 0; zz < w.nsplit; ++zz) {
+        // Partials are summed in split order (deterministic); loads for RG
+        // consecutive splits are issued together so that RG L2 round trips
+        // overlap (RG * DC <= 64 extra registers).
+        constexpr int RG = DC >= 64 ? 1 : 64 / DC;
+        int zz = 0;
+        for (; zz + RG <= w.nsplit; zz += RG) {
+            float pv[RG][DC];
+#pragma unroll
+            for (int g = 0; g < RG; ++g)
+#pragma unroll
+                for (int j = 0; j < DC; ++j) pv[g][j] = __ldcg(base + ((size_t)(zz + g) * BN + c_begin + j) * TM_M + row);
+#pragma unroll
+            for (int g = 0; g < RG; ++g)
+#pragma unroll
+                for (int j = 0; j < DC; ++j) acc[j] += pv[g][j];
+        }
+        for (; zz < w.nsplit; ++zz) {
 #pragma unroll
             for (int j = 0; j < DC; ++j) acc[j] += __ldcg(base + ((size_t)zz * BN + c_begin + j) * TM_M + row);
         }
