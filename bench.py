@@ -219,7 +219,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(c["seconds"] for c in vals), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD if not prec else WORKLOAD.replace(", fp32", ", bf16 operands / fp32 accumulate"), "global_batch": "1,5,20", "parallelism": "host cores",
+            "config": {"workload": WORKLOAD, "global_batch": "1,5,20", "parallelism": "host cores",
                        "sample": cb["sample"]},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cb["cores"], "kind": "port",
                              "sample": cb["sample"]},
@@ -447,6 +447,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook for the N > 1 control flow on a one-GPU box: every rank on cuda:0,
+    # collectives over gloo (NCCL refuses two ranks on one GPU).  Never set by the driver.
+    if os.environ.get("B2C_BENCH_ONE_GPU_TEST") == "1":
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -455,7 +459,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("B2C_BENCH_ONE_GPU_TEST") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -70,3 +70,23 @@ def test_gather_batch_gloo_world2(n_total):
     want = torch.arange(n_total, dtype=torch.float32).view(n_total, 1, 1, 1).expand(n_total, 3, 2, 2)
     for r in range(world):
         assert torch.equal(results[r], want)
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """The driver's reference arm (bench.py --impl reference) needs no GPU: the
+    oracle port timed on host cores, one JSON line from rank 0, silent other ranks."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "0",
+           "--batches", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "TFLOP/s"
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode == 0 and out.stdout.strip() == ""
