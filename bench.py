@@ -45,7 +45,7 @@ METRIC = "conv TFLOP/s + runtime per op, AlexNet/NiN/GoogLeNet sweep at N=1/5/20
 WORKLOAD = "alexnet+nin+googlenet conv sweep: 43 corpus ops x N in {1,5,20}, fused bias+ReLU, fp32"
 
 
-E2E_STREAMS = 3
+E2E_STREAMS = int(os.environ.get("B2C_E2E_STREAMS", "4"))
 
 
 def parse_args():
