@@ -61,7 +61,7 @@ extern "C" {
 #define B2C_VAR_FC 3     /* "conv_fc"    : whole-image filter, weight-streaming GEMM  (variants.py:328-373) */
 #define B2C_VAR_UMMA 4   /* "conv_umma"  : tcgen05/TMEM 3xTF32 implicit GEMM, k x k      (new, B200)       */
 #define B2C_VAR_FC_STREAM 5 /* "conv_fc_stream": fp32 FFMA weight streaming for ConvFC at batch <= 8 (HBM-bound;
-                              reads w once at full bandwidth; mnb0 = warps per block 4|8, mnt1 = rows 2|4)   */
+                              reads w once at full bandwidth; mnb0 = warps per block 2|4|8, mnt1 = rows 2|4|8) */
 
 /* Precision modes. */
 #define B2C_PREC_FP32 0 /* fp32-exact: FFMA, or 3xTF32 split on the tensor cores */

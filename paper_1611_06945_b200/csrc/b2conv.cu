@@ -164,8 +164,8 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             }
             if (d->n > 8) { why = "weight streaming is for batch <= 8 (tensor-core conv_fc beyond)"; return B2C_INAPPLICABLE; }
             if ((d->c * d->r * d->r) % 4) { why = "ic*h*w % 4 != 0 (16-byte rows)"; return B2C_INAPPLICABLE; }
-            if (t->mnb0 != 4 && t->mnb0 != 8) { why = "warps per block (MNb0) must be 4 or 8"; return B2C_INAPPLICABLE; }
-            if (t->mnt1 != 2 && t->mnt1 != 4) { why = "rows per block (MNt1) must be 2 or 4"; return B2C_INAPPLICABLE; }
+            if (t->mnb0 != 2 && t->mnb0 != 4 && t->mnb0 != 8) { why = "warps per block (MNb0) must be 2, 4 or 8"; return B2C_INAPPLICABLE; }
+            if (t->mnt1 != 2 && t->mnt1 != 4 && t->mnt1 != 8) { why = "rows per block (MNt1) must be 2, 4 or 8"; return B2C_INAPPLICABLE; }
             return B2C_OK;
         }
         default:
@@ -742,6 +742,7 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
 #define B2C_FCS(NB_, R_) if (nb == NB_ && R == R_) fn = k_fc_stream<NB_, R_>;
             B2C_FCS(1, 2) B2C_FCS(2, 2) B2C_FCS(4, 2) B2C_FCS(8, 2)
             B2C_FCS(1, 4) B2C_FCS(2, 4) B2C_FCS(4, 4) B2C_FCS(8, 4)
+            B2C_FCS(1, 8) B2C_FCS(2, 8) B2C_FCS(4, 8) B2C_FCS(8, 8)
 #undef B2C_FCS
             if (!fn) return fail(B2C_INAPPLICABLE, "no weight-streaming kernel for this shape");
             const int W = t->mnb0;

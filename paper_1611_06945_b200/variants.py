@@ -302,8 +302,8 @@ class ConvFC(_UmmaFamily):
 
 class ConvFCStream(Variant):
     """ConvFC (variants.py:328-373) as an fp32 FFMA weight-streaming kernel for
-    batch <= 8, where the op is HBM-bound: MNb0 = warps per block (4|8), MNt1 =
-    out_chan rows per block (2|4)."""
+    batch <= 8, where the op is HBM-bound: MNb0 = warps per block (2|4|8), MNt1 =
+    out_chan rows per block (2|4|8; more rows = fewer x re-reads per weight byte)."""
 
     name, rank, vid = "conv_fc_stream", 5, backend.VAR_FC_STREAM
 
@@ -311,7 +311,7 @@ class ConvFCStream(Variant):
         return TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)
 
     def space(self, node, edges):
-        out = [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=1, vw=1) for wp in (4, 8) for r in (2, 4)]
+        out = [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=1, vw=1) for wp in (2, 4, 8) for r in (2, 4, 8)]
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

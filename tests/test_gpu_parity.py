@@ -64,7 +64,8 @@ def _variant_params(g):
                     TuneParams(bn=64, split_k=2, tma=3), TuneParams(bn=96, split_k=0, tma=3), TuneParams(bn=64, tma=3, occ=2)):
             out.append((v, prm))
     out += [("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)),
-            ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1))]
+            ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1)),
+            ("conv_fc_stream", TuneParams(mnt=(1, 8), mnb=(2, 1), kb=1, vw=1))]
     return [(n, p) for n, p in out if VARIANTS[n].applies(node, g.edges, p) is None]
 
 
