@@ -616,10 +616,9 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     } else if (mode == 4) {
         float* xp = reinterpret_cast<float*>(wsb + p.nhwc_off);
         const long long total = (long long)d->n * p.hp * p.wp;
-        const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
         if (!separate) relayout = 2;
         else if (!(g_trace_on & 16)) {
-            cudaError_t le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, 1, x, reinterpret_cast<float4*>(xp),
+            cudaError_t le = launch_pdl(k_to_nhwc4_pad, dim3(d->n * p.hp), dim3(p.wp > 128 ? 256 : 128), 0, st, 1, x, reinterpret_cast<float4*>(xp),
                                         (int)d->c, (int)d->h, (int)d->w, p.hp, p.wp, (int)d->pad, total);
             if (le != cudaSuccess) return cuda_fail(le, "k_to_nhwc4_pad launch");
         }
@@ -634,8 +633,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
             cudaError_t le;
             if (mode == 3) {
                 const long long total = (long long)d->n * HW;
-                const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
-                le = launch_pdl(k_to_nhwc4_pad, dim3(blocks), dim3(256), 0, st, 1, x, reinterpret_cast<float4*>(xh),
+                le = launch_pdl(k_to_nhwc4_pad, dim3(d->n * d->h), dim3(d->w > 128 ? 256 : 128), 0, st, 1, x, reinterpret_cast<float4*>(xh),
                                 (int)d->c, (int)d->h, (int)d->w, (int)d->h, (int)d->w, 0, total);
             } else {
                 dim3 tgrid((HW + 31) / 32, (cp + 31) / 32, d->n);

@@ -277,23 +277,27 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
 // elsewhere: one thread per padded pixel, coalesced plane reads, float4 writes.
 __global__ void __launch_bounds__(256) k_to_nhwc4_pad(const float* __restrict__ x, float4* __restrict__ xp, int C,
                                                       int H, int W, int Hp, int Wp, int pad, long long total) {
+    // one block per padded row (image b, row yq): no per-element index divisions
+    (void)total;
     pdl_launch_dependents();
     pdl_wait();
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int xq = (int)(i % Wp);
-        const long long t = i / Wp;
-        const int yq = (int)(t % Hp);
-        const int b = (int)(t / Hp);
-        const int iy = yq - pad, ix = xq - pad;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if ((unsigned)iy < (unsigned)H && (unsigned)ix < (unsigned)W) {
-            const float* src = x + ((size_t)b * C * H + iy) * W + ix;
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (c < C) v[c] = __ldg(src + (size_t)c * H * W);
+    const int row = blockIdx.x;
+    const int b = row / Hp, yq = row - (row / Hp) * Hp;
+    const int iy = yq - pad;
+    const bool yin = (unsigned)iy < (unsigned)H;
+    const size_t plane = (size_t)H * W;
+    const float* src = x + ((size_t)b * C * H + (yin ? iy : 0)) * W;
+    float4* dst = xp + (size_t)row * Wp;
+    for (int xq = threadIdx.x; xq < Wp; xq += blockDim.x) {
+        const int ix = xq - pad;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (yin && (unsigned)ix < (unsigned)W) {
+            v.x = __ldg(src + ix);
+            if (C > 1) v.y = __ldg(src + plane + ix);
+            if (C > 2) v.z = __ldg(src + 2 * plane + ix);
+            if (C > 3) v.w = __ldg(src + 3 * plane + ix);
         }
-        xp[i] = make_float4(v[0], v[1], v[2], v[3]);
+        dst[xq] = v;
     }
 }
 
