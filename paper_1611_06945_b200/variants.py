@@ -302,8 +302,10 @@ class ConvFC(_UmmaFamily):
 
 class ConvFCStream(Variant):
     """ConvFC (variants.py:328-373) as an fp32 FFMA weight-streaming kernel for
-    batch <= 8, where the op is HBM-bound: MNb0 = warps per block (2|4|8), MNt1 =
-    out_chan rows per block (2|4|8; more rows = fewer x re-reads per weight byte)."""
+    small batch, where the op is HBM-bound.  Kb=1 (batch <= 8): warps split K,
+    x read through L1/L2, MNb0 = warps per block (2|4|8), MNt1 = rows per block
+    (2|4|8).  Kb=2 (batch <= 32): x staged in shared memory per block, MNb0 =
+    warps (4|8), MNt1 = rows per warp (1|2|4)."""
 
     name, rank, vid = "conv_fc_stream", 5, backend.VAR_FC_STREAM
 
@@ -312,6 +314,7 @@ class ConvFCStream(Variant):
 
     def space(self, node, edges):
         out = [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=1, vw=1) for wp in (2, 4, 8) for r in (2, 4, 8)]
+        out += [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=2, vw=1) for wp in (4, 8) for r in (1, 2, 4)]
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

@@ -65,7 +65,10 @@ def _variant_params(g):
             out.append((v, prm))
     out += [("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)),
             ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1)),
-            ("conv_fc_stream", TuneParams(mnt=(1, 8), mnb=(2, 1), kb=1, vw=1))]
+            ("conv_fc_stream", TuneParams(mnt=(1, 8), mnb=(2, 1), kb=1, vw=1)),
+            ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(8, 1), kb=2, vw=1)),
+            ("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(4, 1), kb=2, vw=1)),
+            ("conv_fc_stream", TuneParams(mnt=(1, 1), mnb=(8, 1), kb=2, vw=1))]
     return [(n, p) for n, p in out if VARIANTS[n].applies(node, g.edges, p) is None]
 
 
@@ -213,3 +216,22 @@ def test_bad_args_raise(cuda):
     z = torch.zeros(1024, device="cuda")
     with pytest.raises(ShapeMismatch):
         backend.fwd(d, t, z, z, z, z)
+
+
+@pytest.mark.parametrize("row,batch", [(25, 20), (13, 20), (25, 12), (13, 3), (13, 32)])
+def test_fc_stream_staged_full_size(cuda, row, batch):
+    """conv_fc_stream Kb=2 (x staged in smem) on AlexNet fc6 / fc7 at ragged and large batches."""
+    from paper_1611_06945_b200 import corpus
+    from paper_1611_06945_b200.variants import TuneParams
+
+    op = corpus.corpus(batch)[row]
+    c = {"ksz": op.ksz, "stride": op.stride, "pad": op.pad, "out_chans": op.out_chans,
+         "in": (batch, op.in_chans, op.in_y, op.in_x)}
+    g = _graph(c, True)
+    x, f, b = conv_ref.conv_inputs(batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz, f"fcs:{row}:{batch}")
+    want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
+    tol = conv_ref.tolerance_for(op.in_chans * op.ksz ** 2)
+    for p in (TuneParams(mnt=(1, 2), mnb=(8, 1), kb=2, vw=1), TuneParams(mnt=(1, 1), mnb=(4, 1), kb=2, vw=1)):
+        got = _run_device(g, x, f, b, "conv_fc_stream", p)
+        r = conv_ref.compare(got, want, tol)
+        assert r.ok, (p.to_string(), r)

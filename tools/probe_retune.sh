@@ -1,4 +1,4 @@
-OUT=gpurun_out/m7
+OUT=gpurun_out/m8
 mkdir -p $OUT
 timeout 1200 python -m pytest tests/test_host.py -x -q > $OUT/pytest.log 2>&1; tail -2 $OUT/pytest.log; grep -E "^E " $OUT/pytest.log | head -6
 timeout 2400 python tools/tune_sweep.py --out $OUT/tunedb_b200_fp32.tsv > $OUT/tune.log 2>&1; tail -1 $OUT/tune.log
