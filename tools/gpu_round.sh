@@ -24,3 +24,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_t
 fi
 du -sh $OUT/*
 echo done
+timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "reference exit $?" >> $OUT/bench_reference.err
+timeout 600 python bench.py --prec bf16 --no-cpu > $OUT/bench_bf16.json 2> $OUT/bench_bf16.err
+timeout 600 python tools/net_bench.py > $OUT/net_bench.jsonl 2> $OUT/net_bench.err
