@@ -516,7 +516,11 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
             return;
         }
         if (dtid == 0) {
-            while (ld_acquire_gpu(a.sems + w.t) < w.nsplit - 1) __nanosleep(32);
+            const long long t0 = clock64();
+            while (ld_acquire_gpu(a.sems + w.t) < w.nsplit - 1) {
+                __nanosleep(32);
+                if (clock64() - t0 > (1ll << 32)) __trap();  // a contributor never ran (grid not co-resident)
+            }
             a.sems[w.t] = 0;
         }
         named_bar_sync(1, NT);
