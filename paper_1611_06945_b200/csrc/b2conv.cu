@@ -93,7 +93,7 @@ bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || 
 int window_chunks(const b2c_conv_desc* d) { return (d->r * 4 + TM_BK - 1) / TM_BK; }
 int kmode_for(const b2c_conv_desc* d, int variant, int tma) {
     if (variant == B2C_VAR_FC) return 2;
-    if (tma && tma != 3 && d->c <= 4) return tma == 2 ? 4 : 5;
+    if (tma && tma != 3 && tma != 4 && d->c <= 4) return tma == 2 ? 4 : 5;
     if (variant == B2C_VAR_1X1 || tma) return 3;
     return d->c >= 32 ? 3 : 0;
 }
@@ -180,7 +180,16 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K is single-CTA"; return B2C_INAPPLICABLE; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
-    if (t->tma < 0 || t->tma > 3) { why = "tma must be 0, 1, 2 or 3"; return B2C_BAD_ARGS; }
+    if (t->tma < 0 || t->tma > 4) { why = "tma must be 0..4"; return B2C_BAD_ARGS; }
+    if (t->tma == 4) {  // k x k stride-1 conv read straight from NCHW x (no re-layout launch)
+        if (d->stride != 1 || d->r < 2 || t->variant == B2C_VAR_FC) {
+            why = "tma=4 (direct NCHW k x k) needs a stride-1 conv with ksz >= 2"; return B2C_INAPPLICABLE;
+        }
+        if (t->swap_ab || t->cluster == 2) { why = "tma=4: pixels on M (swap_ab=0), single CTAs"; return B2C_INAPPLICABLE; }
+        if (d->w % 4 || d->ow + 3 > UMMA_M) {
+            why = "tma=4: input width must be a multiple of 4 (16-byte TMA rows) and ow <= 125"; return B2C_INAPPLICABLE;
+        }
+    }
     if (t->tma == 3) {  // 1x1 conv read straight from NCHW x (no re-layout launch)
         if (!(d->r == 1 && d->stride == 1 && d->pad == 0) || t->variant == B2C_VAR_FC) {
             why = "tma=3 (direct NCHW) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
@@ -216,6 +225,7 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
 struct UmmaPlan {
     int grid_x, grid_y, split, kps, kblocks, cblocks, tiles, kmode, flt_rows, tma;
     int bx, by, tiles_x, tiles_y, hp, wp;  // kmode 5: pixel blocks and the padded NHWC extent
+    int box_w;                             // tma = 4: TMA box width (floats) over NCHW rows
     int parts;                             // packed filter halves per K block (2: raw | lo, 1: raw)
     int streamk, sk_grid, sk_maxc;         // split_k == 0: stream-K over the units' K blocks
     size_t wpk_bytes;   // packed filters (offset 0 of the workspace; 0 for the TMA fc path)
@@ -243,7 +253,16 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.kmode = kmode_for(d, t->variant, t->tma);
     p.kblocks = kblocks_for(d, p.kmode);
     p.cblocks = p.kmode == 5 ? window_chunks(d) : (d->c + 31) / 32;
-    p.bx = p.by = p.tiles_x = p.tiles_y = p.hp = p.wp = 0;
+    p.bx = p.by = p.tiles_x = p.tiles_y = p.hp = p.wp = p.box_w = 0;
+    if (t->tma == 4) {  // MODE 6: whole output rows of one image, the box 3+ floats wider for the aligned start
+        p.bx = d->ow;
+        p.box_w = (d->ow + 3 + 3) / 4 * 4;
+        p.by = std::max(1, std::min(UMMA_M / p.box_w, d->oh));
+        p.tiles_x = 1;
+        p.tiles_y = (d->oh + p.by - 1) / p.by;
+        p.grid_x = d->n * p.tiles_y;
+        p.tiles = p.grid_x * p.grid_y;
+    }
     if (t->tma == 3) {  // MODE 5: runs of 128 pixels of one image (tiles do not straddle images)
         p.bx = UMMA_M;
         p.by = 1;
@@ -282,7 +301,7 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.part_off = align256(p.wpk_bytes);
     p.sems_off = p.part_off + (nslots ? align256(nslots * BN * UMMA_M * sizeof(float)) : 0);
     p.nhwc_off = p.sems_off + (nslots ? align256((size_t)p.tiles * sizeof(int)) : 0);
-    const bool nhwc = p.tma && p.tma != 3 && (p.kmode == 3 || p.kmode == 4 || p.kmode == 5);
+    const bool nhwc = p.tma && p.tma != 3 && p.tma != 4 && (p.kmode == 3 || p.kmode == 4 || p.kmode == 5);
     const int cp = p.kmode >= 4 ? 4 : d->c;  // first layers: channels padded to 4 (16-byte pixels)
     const size_t pix = p.kmode == 5 ? (size_t)p.hp * p.wp : (size_t)d->h * d->w;
     p.gbar_off = p.nhwc_off + (nhwc ? align256((size_t)d->n * cp * pix * sizeof(float)) : 0);
@@ -525,7 +544,7 @@ TconvEntry tconv_pick_bf16(int bn) {
 template <bool SWAP, int MODE>
 TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
     if (cl == 2) {
-        if constexpr (!SWAP && MODE != 1 && MODE != 5) {
+        if constexpr (!SWAP && MODE != 1 && MODE != 5 && MODE != 6) {
             switch (bn) {
                 case 64: return tconv_entry<64, false, MODE, 1, 2>();
                 case 96: return tconv_entry<96, false, MODE, 1, 2>();
@@ -565,6 +584,7 @@ TconvEntry tconv_pick(int bn, int swap, int mode, int occ, int cl) {
         case 3: return tconv_pick_sw<3>(bn, swap, occ, cl);
         case 4: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 4>(bn, occ, cl);
         case 5: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 5>(bn, occ, cl);
+        case 6: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 6>(bn, occ, cl);
     }
     return TconvEntry{nullptr, 0, 0};
 }
@@ -585,13 +605,14 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     int rc = load_tma_encoders();
     if (rc) return rc;
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
-    const int mode = t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
+    const int mode = t->tma == 4 ? 6 : t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
     const int cl = t->cluster == 2 ? 2 : 1;
     TconvEntry e{nullptr, 0, 0};
     if (d->prec == B2C_PREC_BF16)
         e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
             : mode == 4 ? tconv_pick_bf16<4>(t->tile_n) : mode == 5 ? tconv_pick_bf16<5>(t->tile_n)
+            : mode == 6 ? tconv_pick_bf16<6>(t->tile_n)
             : TconvEntry{nullptr, 0, 0};
     else
         e = tconv_pick(t->tile_n, t->swap_ab, mode, occ, cl);
@@ -615,6 +636,15 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeTiled (NCHW 1x1) failed (" + std::to_string((int)r) + ")");
+    } else if (mode == 6) {  // k x k, stride 1: x itself as [img][chan][y][x]; box = box_w x by pixels x 32 channels
+        const cuuint64_t dims[4] = {(cuuint64_t)d->w, (cuuint64_t)d->h, (cuuint64_t)d->c, (cuuint64_t)d->n};
+        const cuuint64_t strides[3] = {(cuuint64_t)d->w * 4, (cuuint64_t)d->h * d->w * 4, (cuuint64_t)d->c * d->h * d->w * 4};
+        const cuuint32_t box[4] = {(cuuint32_t)p.box_w, (cuuint32_t)p.by, (cuuint32_t)TM_BK, 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = g_enc_tiled(&tm_pix, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeTiled (NCHW kxk) failed (" + std::to_string((int)r) + ")");
     } else if (mode == 4) {
         float* xp = reinterpret_cast<float*>(wsb + p.nhwc_off);
         const long long total = (long long)d->n * p.hp * p.wp;
@@ -672,6 +702,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.by = p.by;
     a.tiles_x = p.tiles_x;
     a.tiles_y = p.tiles_y;
+    a.box_w = p.box_w;
     a.fCB = FastDiv((uint32_t)p.cblocks);
     a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
     a.ws = reinterpret_cast<float*>(wsb + p.part_off);
@@ -687,7 +718,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.flt_early = t->prepared ? 1 : 0;  // b2c_conv_prepare synchronises, so a prepared pack is complete
     {
         int period = p.kblocks, valid = g.K - TM_BK * (p.kblocks - 1);  // fc (MODE 1): flat K tail
-        if (mode == 0 || mode == 2 || mode == 5) {
+        if (mode == 0 || mode == 2 || mode == 5 || mode == 6) {
             period = p.cblocks;
             valid = d->c - TM_BK * (period - 1);
         } else if (mode == 4) {
@@ -994,7 +1025,7 @@ int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
     if (!t) return 0;
     const int pack = (is_umma(t->variant) && !t->prepared && !(t->tma && t->variant == B2C_VAR_FC)) ? 1 : 0;
     const bool sep = std::getenv("B2C_FUSED_NHWC") == nullptr || (t->tma == 2 && d && d->c <= 4);
-    const int nhwc = (is_umma(t->variant) && t->tma && t->tma != 3 && t->variant != B2C_VAR_FC && sep) ? 1 : 0;
+    const int nhwc = (is_umma(t->variant) && t->tma && t->tma != 3 && t->tma != 4 && t->variant != B2C_VAR_FC && sep) ? 1 : 0;
     return 1 + pack + nhwc;
 }
 

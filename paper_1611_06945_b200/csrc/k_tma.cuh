@@ -79,7 +79,7 @@ constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
     static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && CL == 1), "bf16: pixels on M, packed filters");
-    static_assert(MODE != 5 || CL == 1, "MODE 5: single CTAs");
+    static_assert((MODE != 5 && MODE != 6) || CL == 1, "MODE 5/6: single CTAs");
     static_assert(CL == 1 || (CL == 2 && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
@@ -119,7 +119,7 @@ struct TmaCfg {
     static constexpr bool SW128 = MODE != 3;
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
     static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
-    static_assert(MODE != 5 || !SWAP, "MODE 5 tiles are pixel runs on M (split warps transpose them)");
+    static_assert((MODE != 5 && MODE != 6) || !SWAP, "MODE 5/6 tiles are pixel blocks on M (split warps transpose them)");
     static_assert(STAGES >= 2, "need at least two stages");
     static_assert(DRAIN_COLS % 8 == 0, "TMEM drain granularity");
 };
@@ -154,6 +154,7 @@ struct TArgs {
     // K blocks whose index % kb_period == kb_period - 1 hold only ksteps_last valid
     // groups of 8 K (channel / window / K tail); the MMAs skip the all-zero rest.
     int kb_period, ksteps_last;
+    int box_w;  // MODE 6: box width in floats (multiple of 4, >= bx + 3); the box is [32 ch][by][box_w]
 };
 
 // Walks a CTA's work: units blockIdx, +stride, ... ; or, in stream-K mode, the
@@ -199,7 +200,7 @@ __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     w.n0 = nt * FLT_ROWS;
     w.kb_begin = w.z * a.kps;
     w.nkb = min(a.kblocks, w.kb_begin + a.kps) - w.kb_begin;
-    if (MODE == 4 || MODE == 5) {  // MODE 5: tiles_y = by = 1, bx = 128 (pixel runs of one image)
+    if (MODE == 4 || MODE == 5 || MODE == 6) {  // MODE 5: tiles_y = by = 1, bx = 128 (pixel runs of one image)
         const int per_img = a.tiles_x * a.tiles_y;
         w.b = mt / per_img;
         const int r = mt - w.b * per_img;
@@ -461,10 +462,10 @@ __device__ __forceinline__ void a_to_tmem_bf16(uint32_t a, int tid, uint32_t tco
 // loads at a 512-byte stride (consecutive threads hit consecutive banks).  PREC 0
 // stores raw | lo (3xTF32), PREC 1 packs bf16 pairs.
 template <int PREC>
-__device__ __forceinline__ void a_to_tmem_cmajor(uint32_t a, int tid, uint32_t tcol) {
+__device__ __forceinline__ void a_to_tmem_cmajor(uint32_t a, int idx, uint32_t tcol, int cstride) {
     float v[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) v[c] = lds32(a + (uint32_t)(c * TM_M + tid) * 4u);
+    for (int c = 0; c < 32; ++c) v[c] = lds32(a + (uint32_t)(c * cstride + idx) * 4u);
     if constexpr (PREC == 1) {
         uint32_t r[16];
 #pragma unroll
@@ -554,7 +555,7 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
             const int p = w.ox0 + row;
             if (p >= g.PQ) return;
             row_out = (long long)w.b * g.OC * g.PQ + p;
-        } else if (MODE == 4) {  // rectangular tile: row = y * bx + x
+        } else if (MODE == 4 || MODE == 6) {  // rectangular tile: row = y * bx + x
             const int y = row / a.bx, x = row - (row / a.bx) * a.bx;
             const int oy = w.oy0 + y, ox = w.ox0 + x;
             if (y >= a.by || oy >= g.OH || ox >= g.OW) return;
@@ -690,8 +691,18 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     mbar_wait(smem_u32(&afree_bar[aslot]), (uint32_t)((n / Cfg::A_SLOTS) - 1) & 1u);
                 tc_fence_after();
                 const uint32_t acol = (uint32_t)(Cfg::ACC_COLS + aslot * 64);
-                if (MODE == 5)  // channel-major box [32 ch][128 px]: this thread's pixel is column tid
-                    a_to_tmem_cmajor<PREC>(sbase, tid, t_lane + acol);
+                if (MODE == 5) {  // channel-major box [32 ch][128 px]: this thread's pixel is column tid
+                    a_to_tmem_cmajor<PREC>(sbase, tid, t_lane + acol, TM_M);
+                } else if (MODE == 6) {  // box [32 ch][by][box_w] starting at the 16-byte-aligned x below this tap
+                    uint32_t tap, cb, ky, kx;
+                    a.fCB.divmod((uint32_t)(w.kb_begin + i), tap, cb);
+                    g.fR.divmod(tap, ky, kx);
+                    const int dx = (int)kx - g.P;
+                    const int shift = dx - ((dx >= 0 ? dx : dx - 3) / 4) * 4;  // dx - floor(dx / 4) * 4
+                    const int y = tid / a.bx, xx = tid - (tid / a.bx) * a.bx;
+                    const int idx = y < a.by ? y * a.box_w + xx + shift : 0;  // rows past the tile: any in-box value
+                    a_to_tmem_cmajor<PREC>(sbase, idx, t_lane + acol, a.by * a.box_w);
+                }
                 else if (PREC == 1)
                     a_to_tmem_bf16<Cfg::SW128>(sbase, tid, t_lane + acol);
                 else if (!(a.trace & 8))
@@ -862,7 +873,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 // MODE 4 boxes are bx*by rows (<= 128): the rest of the tile keeps
                 // stale (finite) data whose output rows the epilogue discards.
                 const bool pre = n < npre;  // filter bytes already issued (and counted) for this stage
-                const uint32_t bytes = (MODE == 4 ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u : Cfg::BYTES) -
+                const uint32_t bytes = (MODE == 4   ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u
+                                        : MODE == 6 ? Cfg::BYTES - (uint32_t)(TM_M - a.box_w * a.by) * 128u
+                                                    : Cfg::BYTES) -
                                        (pre ? (uint32_t)Cfg::FLT_STAGE : 0u);
                 mbar_arrive_expect_tx(bar, bytes);
                 if (n < 32) B2C_TRACE(a.trace, 176 + n);
@@ -874,6 +887,13 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                         tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
                     } else if (MODE == 5) {  // (pixel run, channel block, image) straight from NCHW x
                         tma_load_3d(pix, &tm_pix, bar, w.ox0, kb * TM_BK, w.b);
+                    } else if (MODE == 6) {  // (x, y, channel block, image) of NCHW x; x start rounded down to 16 B
+                        uint32_t tap, cb, ky, kx;
+                        a.fCB.divmod((uint32_t)kb, tap, cb);
+                        g.fR.divmod(tap, ky, kx);
+                        const int dx = w.ox0 + (int)kx - g.P;
+                        const int xs = ((dx >= 0 ? dx : dx - 3) / 4) * 4;  // floor to a multiple of 4 floats
+                        tma_load_4d(pix, &tm_pix, bar, xs, w.oy0 + (int)ky - g.P, (int)cb * TM_BK, w.b);
                     } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
                         uint32_t ky, kc;
                         a.fCB.divmod((uint32_t)kb, ky, kc);

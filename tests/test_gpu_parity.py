@@ -61,7 +61,9 @@ def _variant_params(g):
                     TuneParams(bn=32, swap_ab=True, split_k=0, tma=1), TuneParams(bn=64, tma=1, occ=2),
                     TuneParams(bn=32, swap_ab=True, split_k=2, tma=1, occ=2), TuneParams(bn=64, tma=1, cl=2),
                     TuneParams(bn=96, split_k=2, tma=2, cl=2), TuneParams(bn=32, tma=3), TuneParams(bn=128, tma=3),
-                    TuneParams(bn=64, split_k=2, tma=3), TuneParams(bn=96, split_k=0, tma=3), TuneParams(bn=64, tma=3, occ=2)):
+                    TuneParams(bn=64, split_k=2, tma=3), TuneParams(bn=96, split_k=0, tma=3), TuneParams(bn=64, tma=3, occ=2),
+                    TuneParams(bn=32, tma=4), TuneParams(bn=128, split_k=2, tma=4), TuneParams(bn=64, split_k=0, tma=4),
+                    TuneParams(bn=64, tma=4, occ=2)):
             out.append((v, prm))
     out += [("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)),
             ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1)),
@@ -235,3 +237,30 @@ def test_fc_stream_staged_full_size(cuda, row, batch):
         got = _run_device(g, x, f, b, "conv_fc_stream", p)
         r = conv_ref.compare(got, want, tol)
         assert r.ok, (p.to_string(), r)
+
+
+@pytest.mark.parametrize("row,batch", [(0, 2), (29, 1), (31, 3), (39, 2), (41, 1)])
+def test_direct_nchw_kxk_full_size(cuda, row, batch):
+    """tm=4: k x k stride-1 convs read straight from NCHW by 4-D TMA boxes whose x start is
+    rounded down to 16 bytes (the split warps apply the tap's shift): 28x28 / 56x56 GoogLeNet layers."""
+    from paper_1611_06945_b200 import corpus
+    from paper_1611_06945_b200.variants import VARIANTS, TuneParams
+
+    op = corpus.corpus(batch)[row]
+    c = {"ksz": op.ksz, "stride": op.stride, "pad": op.pad, "out_chans": op.out_chans,
+         "in": (batch, op.in_chans, op.in_y, op.in_x)}
+    g = _graph(c, True)
+    x, f, b = conv_ref.conv_inputs(batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz, f"tm4:{row}", low=-1.0, high=1.0)
+    want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
+    bound = conv_ref.signed_bound(x, f, op.stride, op.pad)
+    ran = 0
+    for p in (TuneParams(bn=32, tma=4), TuneParams(bn=64, split_k=2, tma=4), TuneParams(bn=128, split_k=0, tma=4),
+              TuneParams(bn=64, tma=4, occ=2), TuneParams(bn=64, tma=4, prec=1)):
+        if VARIANTS["conv_umma"].applies(g.node("conv"), g.edges, p) is not None:
+            continue
+        got = _run_device(g, x, f, b, "conv_umma", p)
+        err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+        k = 8e-3 if p.prec else 1e-5
+        assert (err <= k * bound + 1e-6).all(), (p.to_string(), float((err / (bound + 1e-30)).max()))
+        ran += 1
+    assert ran >= 4

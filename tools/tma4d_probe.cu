@@ -49,14 +49,14 @@ int main() {
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     printf("encode rc=%d\n", (int)r);
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + nbytes);
-    int coords[3][4] = {{0, 0, 0, 0}, {-1, -1, 0, 0}, {-2, 3, 0, 0}};
+    int coords[6][4] = {{0, 0, 0, 0}, {-4, 0, 0, 0}, {0, -1, 0, 0}, {-4, -2, 0, 0}, {4, 26, 0, 0}, {-1, -1, 0, 0}};
     for (auto& c : coords) {
         k_probe<<<1, 128, 1024 + nbytes>>>(tm, dout, c[0], c[1], c[2], c[3], nbytes);
         cudaError_t e = cudaDeviceSynchronize();
         float h[8];
         cudaMemcpy(h, dout, sizeof(h), cudaMemcpyDeviceToHost);
         printf("coords (%d,%d,%d,%d): %s done=%g first=%g %g %g\n", c[0], c[1], c[2], c[3], cudaGetErrorString(e), h[0], h[1], h[2], h[3]);
-        if (e != cudaSuccess) return 1;
+        if (e != cudaSuccess) return 1;  // sticky: later cases cannot run
     }
     return 0;
 }
