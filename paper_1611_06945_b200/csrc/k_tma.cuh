@@ -498,40 +498,36 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
         named_bar_sync(1, NT);
     }
     if (w.nsplit > 1) {
-        // Owner-based fixup: the contributor holding the tile's first K blocks
-        // (z = 0 — in stream-K the CTA that reaches this tile last) keeps its
-        // partial in registers; every other contributor publishes its partial
-        // to L2, fences and bumps the tile's counter; the owner waits for the
-        // count, resets it (self-resetting for the next launch) and sums the
-        // partials in split order — the same order, so the same bits, as a
-        // plain z = 0..n-1 sum.  Waits only point at higher-numbered units /
-        // the starts of later CTAs' ranges, and all CTAs are co-resident
-        // (grid <= SMs x occupancy), so the wait cannot deadlock.
-        if (w.z != 0) {
-            float* part = a.ws + ((size_t)w.pslot0 + w.z) * BN * TM_M;
+        // Split-K / stream-K fixup: every contributor publishes its fp32 partial
+        // to L2, fences and takes a ticket; the one that arrives last reduces
+        // all partials in split order (deterministic) and resets the ticket.
+        // No CTA ever waits on another, so the fixup is correct whether or not
+        // the grid is co-resident (concurrent kernels on other streams).
+        // (An owner-waits variant saved one L2 round trip but could deadlock
+        // against a concurrent kernel holding the SMs its contributors need.)
+        float* part = a.ws + ((size_t)w.pslot0 + w.z) * BN * TM_M;
 #pragma unroll
-            for (int j = 0; j < DC; ++j) __stcg(part + (size_t)(c_begin + j) * TM_M + row, acc[j]);
-            __threadfence();
-            named_bar_sync(1, NT);
-            if (dtid == 0) atomicAdd(a.sems + w.t, 1);
-            return;
-        }
+        for (int j = 0; j < DC; ++j) __stcg(part + (size_t)(c_begin + j) * TM_M + row, acc[j]);
+        __threadfence();
+        named_bar_sync(1, NT);
         if (dtid == 0) {
-            const long long t0 = clock64();
-            while (ld_acquire_gpu(a.sems + w.t) < w.nsplit - 1) {
-                __nanosleep(32);
-                if (clock64() - t0 > (1ll << 32)) __trap();  // a contributor never ran (grid not co-resident)
-            }
-            a.sems[w.t] = 0;
+            const int ticket = atomicAdd(a.sems + w.t, 1);
+            *last_flag = (ticket == w.nsplit - 1);
         }
         named_bar_sync(1, NT);
+        const bool last = *last_flag != 0;
+        named_bar_sync(1, NT);  // last_flag is rewritten by the next unit
+        if (!last) return;
         __threadfence();
+        if (dtid == 0) a.sems[w.t] = 0;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
         const float* base = a.ws + (size_t)w.pslot0 * BN * TM_M;
         // Partials are summed in split order (deterministic); loads for RG
         // consecutive splits are issued together so that RG L2 round trips
         // overlap (RG * DC <= 64 extra registers).
         constexpr int RG = DC >= 64 ? 1 : 64 / DC;
-        int zz = 1;
+        int zz = 0;
         for (; zz + RG <= w.nsplit; zz += RG) {
             float pv[RG][DC];
 #pragma unroll

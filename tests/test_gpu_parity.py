@@ -264,3 +264,37 @@ def test_direct_nchw_kxk_full_size(cuda, row, batch):
         assert (err <= k * bound + 1e-6).all(), (p.to_string(), float((err / (bound + 1e-30)).max()))
         ran += 1
     assert ran >= 4
+
+
+def test_split_k_ops_concurrent_on_streams(cuda):
+    """Split-K / stream-K launches of several ops overlapping on three streams give
+    the same bits as serial launches (the fixup never waits on another CTA, so
+    concurrent grids cannot deadlock it)."""
+    import torch
+
+    from paper_1611_06945_b200 import corpus, runner
+    from paper_1611_06945_b200.frontend import with_fused
+    from paper_1611_06945_b200.variants import VARIANTS, TuneParams
+
+    ops = []
+    for row, batch, p in ((40, 5, TuneParams(bn=96, split_k=4, tma=1)), (42, 5, TuneParams(bn=128, split_k=0, tma=1)),
+                          (36, 1, TuneParams(bn=32, split_k=8, swap_ab=True, tma=1)), (37, 5, TuneParams(bn=64, split_k=0, tma=1)),
+                          (2, 5, TuneParams(bn=32, split_k=4, tma=2)), (38, 1, TuneParams(bn=32, split_k=4, tma=1))):
+        op = corpus.corpus(batch)[row]
+        g = with_fused(op.graph(), "conv", "relu")
+        node = g.node("conv")
+        inputs = runner.node_test_inputs(node, g.edges, f"conc:{row}")
+        x, w, b = (runner.to_device(inputs[e]) for e in node.inputs)
+        ops.append(runner.ConvOp(VARIANTS["conv_umma" if op.ksz > 1 else "conv_1x1"].generate(node, g.edges, p), x, w, b))
+    ref = []
+    for o in ops:
+        o.launch()
+        torch.cuda.synchronize()
+        ref.append(o.y.clone())
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for _ in range(5):
+        for i, o in enumerate(ops):
+            o.launch(streams[i % 3].cuda_stream)
+    torch.cuda.synchronize()
+    for o, r in zip(ops, ref):
+        assert torch.equal(o.y, r)
