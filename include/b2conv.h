@@ -60,8 +60,10 @@ extern "C" {
 #define B2C_VAR_1X1 2    /* "conv_1x1"   : k=1,pad=0 tcgen05 GEMM                     (variants.py:279-325) */
 #define B2C_VAR_FC 3     /* "conv_fc"    : whole-image filter, weight-streaming GEMM  (variants.py:328-373) */
 #define B2C_VAR_UMMA 4   /* "conv_umma"  : tcgen05/TMEM 3xTF32 implicit GEMM, k x k      (new, B200)       */
-#define B2C_VAR_FC_STREAM 5 /* "conv_fc_stream": fp32 FFMA weight streaming for ConvFC at batch <= 8 (HBM-bound;
-                              reads w once at full bandwidth; mnb0 = warps per block 2|4|8, mnt1 = rows 2|4|8) */
+#define B2C_VAR_FC_STREAM 5 /* "conv_fc_stream": fp32 FFMA weight streaming for ConvFC (HBM-bound at small
+                              batch; reads w once).  kb = 1 (batch <= 8): warps split K, mnb0 = warps per
+                              block 2|4|8, mnt1 = rows per block 2|4|8; kb = 2 (batch <= 32): x staged in
+                              shared memory, mnb0 = warps 4|8, mnt1 = rows per warp 1|2|4 */
 
 /* Precision modes. */
 #define B2C_PREC_FP32 0 /* fp32-exact: FFMA, or 3xTF32 split on the tensor cores */
@@ -101,7 +103,11 @@ typedef struct b2c_tune {
                     1 = TMA-fed persistent kernel (k_tconv): im2col TMA on an NHWC copy of x made
                     in the workspace by the same call (first layers, C <= 4: x-window boxes on a
                     padded NHWC4 copy), or 2-D TMA of raw x / w for conv_fc;
-                    2 = as 1, but 2-D tiles for 1x1/stride-1 convs and 8-tap 16-byte boxes for C <= 4 */
+                    2 = as 1, but 2-D tiles for 1x1/stride-1 convs and 8-tap 16-byte boxes for C <= 4;
+                    3 = 1x1 / stride 1 / pad 0 convs read straight from NCHW x (3-D TMA box
+                        [32 ch][128 px] per K block; h*w*4 bytes a multiple of 16; no re-layout launch);
+                    4 = k x k stride-1 convs read straight from NCHW x (4-D TMA box of whole output
+                        rows, x start rounded down to 16 bytes; input width a multiple of 4) */
     int32_t cluster; /* TMA kernel: 2 = CTA pairs (thread-block clusters) take neighbouring pixel tiles of the
                         same filter tile and multicast each filter stage to both (half the filter L2 traffic);
                         0/1 = single CTAs.  Pairs need swap_ab = 0 and a conv (not fc) variant. */
