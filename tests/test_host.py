@@ -230,3 +230,22 @@ def test_bf16_mode_params_and_applicability():
     cands = tuner.candidates(node, g.edges, prec=1)
     assert cands and all(p.prec == 1 and v.name in ("conv_umma", "conv_1x1") for v, p in cands)
     assert tuner.tolerance_for(9999, prec=1).rel_tol == 4e-3 and tuner.tolerance_for(100).rel_tol == 1e-5
+
+
+def test_direct_nchw_operand_paths_applicability():
+    """tm=3 (1x1 straight from NCHW) and tm=4 (k x k stride 1 straight from NCHW): TMA needs
+    16-byte global strides, so h*w*4 (tm=3) / w*4 (tm=4) must be multiples of 16."""
+    one = g_of(1, 1, 0, 64, (2, 96, 28, 28))       # h*w = 784: ok
+    odd = g_of(1, 1, 0, 64, (2, 96, 13, 13))       # 169: no
+    k3 = g_of(3, 1, 1, 64, (2, 64, 28, 28))        # w = 28: ok
+    k3odd = g_of(3, 1, 1, 64, (2, 64, 27, 27))     # w = 27: no
+    k3s2 = g_of(3, 2, 1, 64, (2, 64, 28, 28))      # stride 2: no
+    ok = lambda g, p: VARIANTS["conv_umma"].applies(g.node("conv"), g.edges, p) is None  # noqa: E731
+    assert ok(one, TuneParams(bn=64, tma=3)) and not ok(odd, TuneParams(bn=64, tma=3))
+    assert not ok(k3, TuneParams(bn=64, tma=3))    # tm=3 is 1x1 only
+    assert ok(k3, TuneParams(bn=64, tma=4)) and not ok(k3odd, TuneParams(bn=64, tma=4))
+    assert not ok(k3s2, TuneParams(bn=64, tma=4)) and not ok(one, TuneParams(bn=64, tma=4))
+    assert not ok(k3, TuneParams(bn=64, tma=4, swap_ab=True))
+    assert ok(k3, TuneParams(bn=64, tma=4, prec=1)) and ok(one, TuneParams(bn=64, tma=3, prec=1))
+    n_tm34 = sum(1 for v, p in tuner.candidates(k3.node("conv"), k3.edges) if p.tma == 4)
+    assert n_tm34 > 0
