@@ -298,3 +298,36 @@ def test_split_k_ops_concurrent_on_streams(cuda):
     torch.cuda.synchronize()
     for o, r in zip(ops, ref):
         assert torch.equal(o.y, r)
+
+
+@pytest.mark.parametrize("row,params", [(38, "BN=96,sk=4,sw=0,dr=0,tm=1"), (2, "BN=32,sk=2,sw=0,dr=0,tm=2"),
+                                        (41, "BN=64,sk=1,sw=0,dr=0,tm=4"), (25, "BN=32,sk=4,sw=1,dr=0,tm=1")])
+def test_batch_slabs_concatenate_bit_identical(cuda, row, params):
+    """batch sharding = contiguous image slabs (shard.batch_slab); with the same
+    kernel choice, running the slabs separately and concatenating gives the single-run bits."""
+    import torch
+
+    from paper_1611_06945_b200 import corpus, runner, shard
+    from paper_1611_06945_b200.frontend import with_fused
+    from paper_1611_06945_b200.variants import VARIANTS, TuneParams
+
+    p = TuneParams.from_string("MNt=4:4,MNb=16:16,Kb=4,vw=4,lf=1,li=1," + params)
+    n = 8
+    full = corpus.corpus(n)[row]
+    g = with_fused(full.graph(), "conv", "relu")
+    node = g.node("conv")
+    inputs = runner.node_test_inputs(node, g.edges, f"slab:{row}")
+    x, w, b = (runner.to_device(inputs[e]) for e in node.inputs)
+    vname = "conv_fc" if row == 25 else ("conv_1x1" if full.ksz == 1 else "conv_umma")
+    whole = runner.ConvOp(VARIANTS[vname].generate(node, g.edges, p), x, w, b)
+    whole.launch()
+    parts = []
+    for rank in range(3):
+        start, count = shard.batch_slab(n, 3, rank)
+        op = full.with_batch(count)
+        gs = with_fused(op.graph(), "conv", "relu")
+        o = runner.ConvOp(VARIANTS[vname].generate(gs.node("conv"), gs.edges, p), x[start:start + count].contiguous(), w, b)
+        o.launch()
+        parts.append(o.y)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, 0), whole.y)
