@@ -165,3 +165,25 @@ def test_graph_exec_replay_is_deterministic(cuda):
     torch.cuda.synchronize()
     for e, t in first.items():
         assert torch.equal(t, ex.buffers[e]), e
+
+
+def test_network_bf16_mode_via_bf16_tunedb(cuda):
+    """The bf16 TuneDB's records carry pr=1, so plan_graph with it runs every conv node in the
+    bf16 mode; each node is checked at the bf16 tolerance (rel 4e-3), pool exactly."""
+    from paper_1611_06945_b200 import runner, tuner
+    from paper_1611_06945_b200.frontend import parse_net
+
+    db = tuner.load_db(tuner.shipped_db_path("bf16"))
+    g = parse_net(open(os.path.join(NETS, "alexnet.net")).read())
+    plan = runner.plan_graph(g, db=db)
+    assert any(p.prec == 1 for v, p in plan.choices.values() if v.startswith("conv_"))
+
+    def check(node, edges, inputs, got):
+        ins = {e: a.to_np() for e, a in inputs.items()}
+        want = net_ref.node_reference(node, edges, ins)
+        tol = conv_ref.Tol(4e-3) if node.kind == "Convolution" else conv_ref.Tol(0.0, 0.0)
+        return conv_ref.compare(got.to_np(), want, tol)
+
+    res = runner.run_graph(g, seed="bf16net", db=db, check=check)
+    bad = {k: v for k, v in res.oracle_checks.items() if not v.ok}
+    assert not bad, bad
