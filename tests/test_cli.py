@@ -65,3 +65,21 @@ def test_bench_on_device_small_corpus(cuda, tmp_path, capsys):
     assert cli.main(["bench", "--corpus", str(p), "--db", db, "--relu"]) == cli.EXIT_OK
     rows = list(csv.reader(io.StringIO(capsys.readouterr().out)))[1:]
     assert len(rows) == 4 and all(r[5] == "pass" and float(r[3]) > 0 and r[4] == "wall" for r in rows)
+
+
+@pytest.mark.gpu
+def test_tune_then_bench_with_the_new_db(cuda, tmp_path, capsys):
+    """cli tune (on-device sweep) writes a boda-tunedb v1 file that cli bench then uses."""
+    ops = [op.with_batch(1) for op in corpus.corpus()[2:4]]
+    p = tmp_path / "c.csv"
+    p.write_text(corpus.to_csv(ops))
+    db = tmp_path / "db.tsv"
+    assert cli.main(["tune", "--corpus", str(p), "--out", str(db)]) == cli.EXIT_OK
+    text = db.read_text().splitlines()
+    assert text[0] == "boda-tunedb v1" and len(text) == 3 and all(line.endswith("\twall") for line in text[1:])
+    capsys.readouterr()
+    assert cli.main(["bench", "--corpus", str(p), "--db", str(db)]) == cli.EXIT_OK
+    rows = list(csv.reader(io.StringIO(capsys.readouterr().out)))[1:]
+    recs = dict(line.split("\t")[:2] for line in text[1:])  # the DB file is sorted by signature
+    assert {r[0]: r[1] for r in rows} == recs
+    assert all(r[5] == "pass" for r in rows)
