@@ -130,8 +130,11 @@ int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, 
 
 /* Device workspace bytes b2c_conv_fwd needs (packed filters + split-K partials + semaphores
  * + the NHWC copy of x for the TMA conv path).
- * The workspace must be zero-filled once before first use (semaphores reset
- * themselves after every launch). */
+ * The workspace MUST be zero-filled once before first use (e.g. cudaMemset after
+ * cudaMalloc): the split-K / stream-K tickets in it are counted up by the
+ * contributing CTAs and reset to zero by the last one, so garbage there makes
+ * the last-arriver reduction misfire and the output silently wrong.  One
+ * workspace per concurrently running launch (tickets are per workspace). */
 size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t);
 
 /* y = act(conv(x, w) + bias), written in place into caller-allocated y
@@ -152,7 +155,11 @@ int b2c_conv_time(const b2c_conv_desc* d, const b2c_tune* t, const float* x, con
 /* End-to-end call over HOST buffers: copies x, w, bias host->device, runs the
  * variant, copies y device->host, all on `stream`, using device scratch the
  * caller provides (dev_scratch of scratch_bytes >= b2c_conv_host_scratch()).
- * This is execute_node (runner.py:73-106) with host NdArrays in and out. */
+ * This is execute_node (runner.py:73-106) with host NdArrays in and out.
+ * dev_scratch may be uninitialised device memory (plain cudaMalloc): the call
+ * zeroes the ticket / barrier words of the workspace part on `stream` itself
+ * before the launch, and packs the filters it just copied (tune.prepared is
+ * ignored).  Host buffers should be pinned for asynchronous copies. */
 size_t b2c_conv_host_scratch(const b2c_conv_desc* d, const b2c_tune* t);
 int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx, const float* hw,
                       const float* hbias, float* hy, void* dev_scratch, size_t scratch_bytes,
@@ -170,6 +177,15 @@ int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t);
 
 /* Thread-local message for the last non-zero status. */
 const char* b2c_last_error(void);
+
+/* Device memory / stream helpers for callers without a CUDA runtime binding of
+ * their own (the reference is numpy-only; integration/cuclgen_b200.py binds
+ * these with ctypes).  b2c_device_alloc returns zero-filled device memory
+ * (cudaMalloc + cudaMemset; NULL and b2c_last_error() on failure) — usable as
+ * dev_scratch for b2c_conv_fwd_host or as a b2c_conv_fwd workspace. */
+void* b2c_device_alloc(size_t bytes);
+int b2c_device_free(void* p);
+int b2c_stream_synchronize(void* stream); /* cudaStreamSynchronize; NULL = legacy default stream */
 
 /* Library version string ("b2conv <semver> sm_100a"). */
 const char* b2c_version(void);

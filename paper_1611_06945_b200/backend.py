@@ -41,6 +41,9 @@ EXPORTS = (
     "b2c_conv_launches",
     "b2c_last_error",
     "b2c_version",
+    "b2c_device_alloc",
+    "b2c_device_free",
+    "b2c_stream_synchronize",
     "b2c_pool_max_fwd",
     "b2c_relu_fwd",
     "b2c_xpose",
@@ -104,6 +107,10 @@ def lib():
         L.b2c_xpose.argtypes = [P(XposeDesc), vp, vp, vp]
         L.b2c_last_error.restype = ctypes.c_char_p
         L.b2c_version.restype = ctypes.c_char_p
+        L.b2c_device_alloc.argtypes = [sz]
+        L.b2c_device_alloc.restype = vp
+        L.b2c_device_free.argtypes = [vp]
+        L.b2c_stream_synchronize.argtypes = [vp]
         _lib = L
     return _lib
 

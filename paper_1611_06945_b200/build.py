@@ -7,6 +7,7 @@ its own sources changed) and linked into one shared library:
 
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 
@@ -36,8 +37,36 @@ def sources() -> list:
     return out
 
 
+def _digest(deps, extra=()) -> str:
+    """sha256 over the dependency files' contents and the compiler flags."""
+    h = hashlib.sha256()
+    for part in (*NVCC_FLAGS, *extra):
+        h.update(part.encode() + b"\0")
+    for path in sorted(deps):
+        h.update(os.path.basename(path).encode() + b"\0")
+        with open(path, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+def _stamp_path(target: str) -> str:
+    return target + ".sha256"
+
+
 def _newer(target: str, deps) -> bool:
-    return os.path.exists(target) and all(os.path.getmtime(s) <= os.path.getmtime(target) for s in deps)
+    """Up to date = the target exists and was built from exactly these source
+    contents and flags (content hash, not mtimes: a copied tree has arbitrary
+    mtimes, so an mtime gate could keep a stale library)."""
+    stamp = _stamp_path(target)
+    if not (os.path.exists(target) and os.path.exists(stamp)):
+        return False
+    with open(stamp) as fh:
+        return fh.read().strip() == _digest(deps)
+
+
+def _write_stamp(target: str, digest: str) -> None:
+    with open(_stamp_path(target), "w") as fh:
+        fh.write(digest + "\n")
 
 
 def up_to_date() -> bool:
@@ -61,11 +90,17 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     for name, (main, deps) in units().items():
         obj = os.path.join(OBJDIR, name)
         if force or not _newer(obj, deps):
+            digest = _digest(deps)  # of the sources as compiled (taken before nvcc reads them)
             _run([nvcc, *NVCC_FLAGS, "-c", "-o", obj + ".tmp", main], verbose)
             os.replace(obj + ".tmp", obj)
+            _write_stamp(obj, digest)
         objs.append(obj)
+    digest = _digest(sources())
+    if any(not _newer(o, d) for o, (_, d) in zip(objs, units().values())):
+        raise RuntimeError("sources changed during the build; run it again")
     _run([nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB + ".tmp", *objs], verbose)
     os.replace(LIB + ".tmp", LIB)
+    _write_stamp(LIB, digest)
     return LIB
 
 

@@ -64,15 +64,16 @@ def _write(args, rows):
         csv.writer(sys.stdout, lineterminator="\n").writerows(rows)
 
 
-def device_check(node, edges, x, w, b, y, seed="check"):
+def device_check(node, edges, x, w, b, y, seed="check", prec: int = 0):
     """(ok, max_rel_err) of a conv output ``y`` against the exact-order
-    conv_simple kernel on the same device operands."""
+    conv_simple kernel on the same device operands, at the tolerance of the
+    precision mode the output was computed in (``TuneParams.prec``)."""
     import torch
 
     ref = runner.ConvOp(VARIANTS["conv_simple"].generate(node, edges, TuneParams()), x, w, b)
     ref.launch()
     torch.cuda.synchronize()
-    tol = tuner.tolerance_for(runner.conv_reduction_terms(node, edges))
+    tol = tuner.tolerance_for(runner.conv_reduction_terms(node, edges), prec)
     return tuner.device_compare(y, ref.y, tol)
 
 
@@ -102,7 +103,7 @@ def cmd_bench(args) -> int:
         x, w, b = (runner.to_device(inputs[e]) for e in node.inputs)
         op_dev = runner.ConvOp(variant.generate(node, g.edges, params, STATIC), x, w, b)
         op_dev.launch()
-        ok, err = device_check(node, g.edges, x, w, b, op_dev.y)
+        ok, err = device_check(node, g.edges, x, w, b, op_dev.y, prec=params.prec)
         ms = op_dev.time_ms(warmup=2, reps=5, l2_flush=True)
         failures += 0 if ok else 1
         rows.append([sig, variant.name, params.to_string(), f"{ms * 1e6:.0f}", tuner.WALL, "pass" if ok else "fail",
@@ -150,7 +151,8 @@ def cmd_run(args) -> int:
         if node.kind != KIND_CONV:
             return None
         x, w, b = (runner.to_device(inputs[e]) for e in node.inputs)
-        return device_check(node, edges, x, w, b, runner.to_device(got))
+        prec = select_variant(node, edges, db)[1].prec  # the mode run_graph's plan chose for this node
+        return device_check(node, edges, x, w, b, runner.to_device(got), prec=prec)
 
     res = runner.run_graph(g, seed=args.seed, db=db, check=check if args.check else None, fuse=not args.no_fuse)
     for nr in res.node_runs:

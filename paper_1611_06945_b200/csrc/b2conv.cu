@@ -369,18 +369,30 @@ int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* w
     return B2C_OK;
 }
 
-// Per-device "max dynamic smem" attribute is set once per kernel.
+// Per-device "max dynamic smem" attribute of a kernel: the largest size set so
+// far is remembered per (kernel, device) and raised whenever a launch needs
+// more (k_tiled<MT,NT> / the staged fc kernels take runtime-dependent sizes).
+struct AttrRec {
+    const void* fn;
+    int dev;
+    int bytes;
+};
 std::mutex g_attr_mu;
-std::vector<std::pair<const void*, int>> g_attr_done;  // (fn, device)
+std::vector<AttrRec> g_attr_done;
 
 int ensure_smem_attr(const void* fn, int bytes) {
     int dev = 0;
     B2C_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_attr_mu);
+    AttrRec* rec = nullptr;
     for (auto& e : g_attr_done)
-        if (e.first == fn && e.second == dev) return B2C_OK;
+        if (e.fn == fn && e.dev == dev) rec = &e;
+    if (rec && rec->bytes >= bytes) return B2C_OK;
     B2C_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    g_attr_done.emplace_back(fn, dev);
+    if (rec)
+        rec->bytes = bytes;
+    else
+        g_attr_done.push_back(AttrRec{fn, dev, bytes});
     return B2C_OK;
 }
 
@@ -998,6 +1010,16 @@ int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx
     float* dy = reinterpret_cast<float*>(p); p += al(yb);
     void* ws = p;
     const size_t wsb = b2c_conv_workspace(d, t);
+    // The split-K / stream-K tickets and the grid-barrier counter must be zero at
+    // rest; the scratch may be fresh (uninitialised) device memory, so zero them
+    // on the stream (a few bytes; the partials themselves need no init).
+    if (wsb && is_umma(t->variant)) {
+        const UmmaPlan up = umma_plan(d, t);
+        if (up.nhwc_off > up.sems_off)
+            B2C_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ws) + up.sems_off, 0, up.nhwc_off - up.sems_off, st));
+        if (up.ws_bytes > up.gbar_off)
+            B2C_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ws) + up.gbar_off, 0, up.ws_bytes - up.gbar_off, st));
+    }
     B2C_CUDA(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, st));
     B2C_CUDA(cudaMemcpyAsync(dw, hw, wb, cudaMemcpyHostToDevice, st));
     B2C_CUDA(cudaMemcpyAsync(db, hbias, bb, cudaMemcpyHostToDevice, st));
@@ -1030,6 +1052,33 @@ int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
 }
 
 const char* b2c_last_error(void) { return g_last_error.c_str(); }
+
+void* b2c_device_alloc(size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaMalloc");
+        return nullptr;
+    }
+    e = cudaMemset(p, 0, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaMemset");
+        cudaFree(p);
+        return nullptr;
+    }
+    return p;
+}
+
+int b2c_device_free(void* p) {
+    if (!p) return B2C_OK;
+    B2C_CUDA(cudaFree(p));
+    return B2C_OK;
+}
+
+int b2c_stream_synchronize(void* stream) {
+    B2C_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+    return B2C_OK;
+}
 
 /* Debug only (not part of include/b2conv.h): enable the phase trace of the
  * TMA kernel's CTA 0 and read it back (256 clock64 stamps). */

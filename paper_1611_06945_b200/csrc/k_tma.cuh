@@ -367,7 +367,14 @@ __device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
     if (threadIdx.x == 0) {
         const unsigned long long ticket = atomicAdd(a.gbar, 1ull);
         const unsigned long long target = (ticket / gridDim.x + 1ull) * gridDim.x;
-        while (ld_acquire_u64(a.gbar) < target) __nanosleep(64);
+        // Needs every CTA of the grid co-resident (grid <= #SMs, 1 CTA/SM) and no
+        // concurrent kernel holding SMs: opt-in (B2C_FUSED_NHWC) experiments only.
+        // Bounded like mbar_wait: a grid that is not co-resident faults instead of hanging.
+        const long long t0 = clock64();
+        while (ld_acquire_u64(a.gbar) < target) {
+            __nanosleep(64);
+            if (clock64() - t0 > (1ll << 32)) __trap();
+        }
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();

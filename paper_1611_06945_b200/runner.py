@@ -232,12 +232,13 @@ class RunResult:
         self.sink_buffers = {} if self.sink_buffers is None else self.sink_buffers
 
 
-def plan_graph(g, db=None, fuse: bool = True) -> ExecPlan:
+def plan_graph(g, db=None, fuse: bool = True, prec: int | None = None) -> ExecPlan:
     """fuse_activations, per-node select_variant + generate, insert_conversions
     for the variants' required formats (Xpose nodes for the conversions), then
-    schedule and allocate (runner.py:155-193)."""
+    schedule and allocate (runner.py:155-193).  ``prec`` pins the conv nodes'
+    precision mode (None: whatever the DB records say)."""
     from . import graphopt
-    from .frontend import KIND_CONVERT, KIND_INPUT
+    from .frontend import KIND_CONV, KIND_CONVERT, KIND_INPUT
     from .variants import DEFAULT_TUNE, VARIANTS, select_variant
 
     if fuse:
@@ -246,7 +247,7 @@ def plan_graph(g, db=None, fuse: bool = True) -> ExecPlan:
     for n in g.nodes:
         if n.kind == KIND_INPUT:
             continue
-        v, p = select_variant(n, g.edges, db)
+        v, p = select_variant(n, g.edges, db, prec=prec if n.kind == KIND_CONV else None)
         choices[n.name] = (v, p)
         fmts[n.name] = v.required_formats(n, g.edges, p)
         insts[n.name] = v.generate(n, g.edges, p, STATIC)
@@ -321,7 +322,8 @@ class GraphExec:
         return sum(op.flops for op in self.ops.values())
 
 
-def run_graph(g, seed=0, db=None, check=None, fuse: bool = True, engine=None, keep_sinks: bool = False) -> RunResult:
+def run_graph(g, seed=0, db=None, check=None, fuse: bool = True, engine=None, keep_sinks: bool = False,
+              prec: int | None = None) -> RunResult:
     """Execute a whole graph on the B200 (runner.py:200-249): plan, allocate,
     fill sources with seeded noise, launch every node in schedule order (each
     timed with CUDA events into its CostReport), then checksum the sinks.
@@ -336,7 +338,7 @@ def run_graph(g, seed=0, db=None, check=None, fuse: bool = True, engine=None, ke
     torch = _torch()
     from dataclasses import replace as dc_replace
 
-    plan = plan_graph(g, db=db, fuse=fuse)
+    plan = plan_graph(g, db=db, fuse=fuse, prec=prec)
     ex = GraphExec(plan, seed)
     res = RunResult(checksums={})
     for name in plan.order:

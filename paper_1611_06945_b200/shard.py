@@ -65,3 +65,100 @@ def gather_batch(y_local, n_total: int, group=None, dst_all: bool = True):
     parts = [torch.empty_like(padded) for _ in range(world)]
     dist.all_gather(parts, padded, group=group)
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+
+
+# ----------------------------------------------------------------------------- sweep partition + gather
+
+
+class WorkItem:
+    """One rank's share of one sweep unit (op at a batch size): images
+    [first, first + count) of the unit's batch, run on ``rank``."""
+
+    __slots__ = ("unit", "rank", "first", "count")
+
+    def __init__(self, unit: int, rank: int, first: int, count: int):
+        self.unit, self.rank, self.first, self.count = unit, rank, first, count
+
+    def __repr__(self):
+        return f"WorkItem(unit={self.unit}, rank={self.rank}, first={self.first}, count={self.count})"
+
+    def __eq__(self, other):
+        return isinstance(other, WorkItem) and (self.unit, self.rank, self.first, self.count) == (
+            other.unit, other.rank, other.first, other.count)
+
+
+def plan_sweep(batch_sizes, world: int, cost=None) -> list:
+    """Strong-scaling partition of the sweep's units over
+    ``world`` ranks, identical on every rank (deterministic):
+
+    * a unit whose batch is >= world is cut into ``world`` contiguous slabs
+      (batch_slab: 20 images over 8 GPUs -> 3,3,3,3,2,2,2,2), one per rank; when
+      the slabs are uneven the larger ones go to the least-loaded ranks (so the
+      extra images rotate over the ranks from unit to unit);
+    * a smaller batch is cut into single images (a batch-1 unit stays whole)
+      and those pieces go longest-first to the least-loaded rank (LPT over the
+      load the slabs already put on each rank).
+
+    ``cost(unit, count)`` estimates a piece's time (default: its image count).
+    Returns WorkItems ordered by unit, then first image."""
+    cost = cost or (lambda unit, count: float(count))
+    items, loads = [], [0.0] * world
+    small = []
+    for u, b in enumerate(batch_sizes):
+        if b >= world:
+            by_load = sorted(range(world), key=lambda k: (loads[k], k))
+            for k in range(world):  # slab k (the larger ones first) -> k-th least-loaded rank
+                first, count = batch_slab(b, world, k)
+                r = by_load[k]
+                items.append(WorkItem(u, r, first, count))
+                loads[r] += cost(u, count)
+        else:
+            small.extend((u, i, 1) for i in range(b))
+    for u, first, count in sorted(small, key=lambda p: (-cost(p[0], p[2]), p[0], p[1])):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        items.append(WorkItem(u, r, first, count))
+        loads[r] += cost(u, count)
+    items.sort(key=lambda it: (it.unit, it.first))
+    return items
+
+
+def gather_to_root(items, local_out: dict, full_out: dict, rank: int, group=None, stage_cpu: bool = False):
+    """Move every slab computed off rank 0 into rank 0's full output tensors:
+    point-to-point sends (owner -> 0) and receives (0 <- owner) of the
+    contiguous NCHW slabs, issued as one batch (NCCL groups them; they run on
+    NCCL's stream after the work already queued on the current stream, so the
+    transfers overlap whatever the caller queues next).
+
+    ``items``: the same WorkItem list on every rank (a group of the sweep);
+    ``local_out[i]``: this rank's output slab for items[i] (owner ranks);
+    ``full_out[unit]``: rank 0's full output of a unit (images on dim 0).
+    Returns the async works (wait() them before reading full_out).  With
+    ``stage_cpu`` (gloo, which cannot send CUDA tensors) the transfers are
+    synchronous through host copies."""
+    import torch.distributed as dist
+
+    ops, post = [], []
+    for i, it in enumerate(items):
+        if it.rank == 0:
+            continue
+        if rank == it.rank:
+            t = local_out[i]
+            ops.append(dist.P2POp(dist.isend, t.cpu() if stage_cpu else t, 0, group))
+        elif rank == 0:
+            dst = full_out[it.unit][it.first: it.first + it.count]
+            if stage_cpu:
+                buf = dst.cpu()
+                ops.append(dist.P2POp(dist.irecv, buf, it.rank, group))
+                post.append((dst, buf))
+            else:
+                ops.append(dist.P2POp(dist.irecv, dst, it.rank, group))
+    if not ops:
+        return []
+    works = dist.batch_isend_irecv(ops)
+    if stage_cpu:
+        for w in works:
+            w.wait()
+        for dst, buf in post:
+            dst.copy_(buf)
+        return []
+    return works

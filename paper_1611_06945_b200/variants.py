@@ -397,17 +397,33 @@ def variants_for_kind(kind: str) -> list:
     return sorted((v for v in VARIANTS.values() if v.kind == kind), key=lambda v: -v.rank)
 
 
-def select_variant(node: OpNode, edges, db=None):
+def select_variant(node: OpNode, edges, db=None, prec: int | None = None):
     """(variant, params) for one node: the TuneDB record for its signature if
-    present, else the most specialized applicable variant (variants.py:840-856)."""
+    present, else the most specialized applicable variant (variants.py:840-856).
+
+    ``prec`` (None = whatever the record says) asks for one precision mode: a
+    record of another mode is not used (op_signature carries no precision, so a
+    bf16 DB handed to an fp32 run must not silently switch the arithmetic), and
+    the heuristic's choice is re-targeted to that mode (first applicable
+    candidate of the mode when the heuristic tile does not apply in it)."""
+    from dataclasses import replace
+
     if db is not None:
         from .tuner import op_signature
 
         rec = db.records.get(op_signature(node, edges))
-        if rec is not None:
+        if rec is not None and (prec is None or rec.params.prec == prec):
             return VARIANTS[rec.variant], rec.params
     for v in variants_for_kind(node.kind):
         params = v.default_params(node, edges)
+        if prec is not None and node.kind == KIND_CONV and params.prec != prec:
+            params = replace(params, prec=prec)
         if v.applies(node, edges, params) is None:
             return v, params
-    raise Inapplicable(f"no variant for node '{node.name}' of kind {node.kind}")
+    if prec:  # no heuristic tile applies in this mode: the first applicable candidate of the mode
+        for v in variants_for_kind(node.kind):
+            for params in with_prec(v.space(node, edges) if hasattr(v, "space") else [], prec):
+                if v.applies(node, edges, params) is None:
+                    return v, params
+    raise Inapplicable(f"no variant for node '{node.name}' of kind {node.kind}" +
+                       (f" in precision mode {prec}" if prec else ""))

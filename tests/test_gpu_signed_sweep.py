@@ -1,0 +1,79 @@
+"""Signed-input parity of the production configuration: all 129 sweep ops (43
+corpus rows x N = 1/5/20) on U[-1, 1) operands, each on the kernel and tile the
+SHIPPED TuneDB selects (fp32 DB, then the bf16 DB), two seeds.
+
+The reference's own data (U[0.1, 1), cuclgen/oracle.py:53-60) makes every
+conv output positive, so ReLU never clips on it (SURVEY.md §8(c) caveat; the
+reference's fused == separate test, tests/test_variants.py:203-210, inherits
+that).  Here about half the outputs are negative, so the fused ReLU epilogue
+of every tuned path (im2col TMA, direct-NCHW 1x1 / k x k, first-layer x-window,
+fc swap, weight streaming, split-K and stream-K fixups) must clip.
+
+Stated tolerances (cancellation makes a pure relative bound meaningless):
+  fp32 mode: |a - b| <= 1e-5 * sum|x||w| + 1e-6
+  bf16 mode: |a - b| <= 8e-3 * sum|x||w| + 1e-6
+and the clipped set must match exactly: an output whose true value is below
+-bound is exactly 0, and an output reported as 0 has a true value <= bound.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import conv_ref
+
+pytestmark = pytest.mark.gpu
+
+SEEDS = ("signed-a", "signed-b")
+
+
+def _sweep_choices(prec):
+    from paper_1611_06945_b200 import corpus, tuner
+    from paper_1611_06945_b200.frontend import with_fused
+    from paper_1611_06945_b200.variants import select_variant
+
+    db = tuner.load_db(tuner.shipped_db_path("bf16" if prec else "fp32"))
+    out = []
+    for row, op in corpus.sweep_ops([1, 5, 20]):
+        g = with_fused(op.graph(), "conv", "relu")
+        node = g.node("conv")
+        sig = tuner.op_signature(node, g.edges)
+        assert sig in db.records, f"shipped DB lacks {sig}"
+        v, p = select_variant(node, g.edges, db, prec=prec)
+        assert p.prec == prec
+        out.append((row, op, node, g.edges, v, p))
+    return out
+
+
+@pytest.mark.parametrize("prec", [0, 1], ids=["fp32_db", "bf16_db"])
+def test_sweep_signed_inputs_shipped_db(cuda, prec):
+    import torch
+
+    from paper_1611_06945_b200 import runner
+
+    k = 8e-3 if prec else 1e-5
+    failures, clipped_total, variants_seen = [], 0, set()
+    for row, op, node, edges, v, p in _sweep_choices(prec):
+        plan = v.generate(node, edges, p)
+        variants_seen.add((v.name, p.tma, p.split_k != 1))
+        for seed in SEEDS:
+            x, f, b = conv_ref.conv_inputs(op.batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz,
+                                           f"{seed}:{row}:{op.batch}", low=-1.0, high=1.0)
+            cop = runner.ConvOp(plan, *(torch.from_numpy(a).cuda() for a in (x, f, b)))
+            cop.y.fill_(float("nan"))
+            cop.launch()
+            torch.cuda.synchronize()
+            got = cop.y.cpu().numpy().astype(np.float64)
+            pre = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=False).astype(np.float64)
+            want = np.maximum(pre, 0.0)
+            bound = k * conv_ref.signed_bound(x, f, op.stride, op.pad) + 1e-6
+            err = np.abs(got - want)
+            bad = ~(err <= bound)  # NaN-safe
+            must_clip = pre < -bound
+            clipped_total += int(must_clip.sum())
+            if bad.any() or (got[must_clip] != 0.0).any() or (pre[got == 0.0] > bound[got == 0.0]).any():
+                failures.append((row, op.batch, seed, v.name, p.to_string(), int(bad.sum()),
+                                 float(np.nanmax(err / bound))))
+            del cop
+    assert not failures, failures[:10]
+    assert clipped_total > 0  # ReLU really clipped
+    assert len(variants_seen) >= 3

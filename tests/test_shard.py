@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1611_06945_b200.shard import batch_slab, gather_batch, lpt_assign
+from paper_1611_06945_b200.shard import WorkItem, batch_slab, gather_batch, gather_to_root, lpt_assign, plan_sweep
 
 
 def test_batch_slabs_cover_and_balance():
@@ -74,7 +74,8 @@ def test_gather_batch_gloo_world2(n_total):
 
 def test_bench_reference_arm_runs_on_cpu():
     """The driver's reference arm (bench.py --impl reference) needs no GPU: the
-    oracle port timed on host cores, one JSON line from rank 0, silent other ranks."""
+    reference's own ref_conv (baseline/_ref; the oracle port when that is not
+    installed) timed on host cores, one JSON line from rank 0, silent other ranks."""
     import json
     import subprocess
     import sys
@@ -86,7 +87,96 @@ def test_bench_reference_arm_runs_on_cpu():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "TFLOP/s"
-    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    ref_installed = os.path.isdir(os.path.join(root, "baseline", "_ref", "site", "cuclgen"))
+    assert line["cpu_baseline"]["kind"] == ("reference" if ref_installed else "port")
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["config"]["ops_per_step"] == 43
+    assert line["cpu_baseline"]["cores"] >= 1 and line["cpu_baseline"]["cpu_model"]
     env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_plan_sweep_covers_every_image_once_and_balances():
+    from paper_1611_06945_b200 import corpus
+
+    sweep = corpus.sweep_ops([1, 5, 20])
+    batches = [op.batch for _, op in sweep]
+    costs = [op.flops_computed / op.batch for _, op in sweep]
+    for world in (1, 2, 4, 8):
+        items = plan_sweep(batches, world, lambda u, c: costs[u] * c)
+        for u, b in enumerate(batches):
+            mine = sorted((it.first, it.count) for it in items if it.unit == u)
+            pos = 0
+            for first, count in mine:  # contiguous, disjoint, complete
+                assert first == pos and count >= 1
+                pos += count
+            assert pos == b
+            if b >= world:  # north_star config 5: one batch_slab per rank (20 over 8 -> 3,3,3,3,2,2,2,2)
+                mine_u = [it for it in items if it.unit == u]
+                assert [it.count for it in mine_u] == [batch_slab(b, world, k)[1] for k in range(world)]
+                assert sorted(it.rank for it in mine_u) == list(range(world))
+        loads = [sum(costs[it.unit] * it.count for it in items if it.rank == r) for r in range(world)]
+        assert max(loads) <= sum(loads) / world + max(costs)  # LPT bound
+        assert items == plan_sweep(batches, world, lambda u, c: costs[u] * c)  # deterministic
+    assert [(it.rank, it.count) for it in plan_sweep([20], 8)] == [(r, 3 if r < 4 else 2) for r in range(8)]
+    assert [(it.rank, it.count) for it in plan_sweep([20, 20], 8)][8:] == [(r, 3 if r >= 4 else 2) for r in
+                                                                            (4, 5, 6, 7, 0, 1, 2, 3)]
+
+
+def _p2p_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        batches = [20, 5, 1, 3]
+        items = plan_sweep(batches, world)
+        full = {u: torch.full((b, 2, 3, 3), -1.0) for u, b in enumerate(batches)} if rank == 0 else {}
+        local = {}
+        for i, it in enumerate(items):
+            if it.rank != rank:
+                continue
+            # image j of unit u holds 100*u + j, computed by its owner
+            y = (100.0 * it.unit + torch.arange(it.first, it.first + it.count, dtype=torch.float32)).view(-1, 1, 1, 1)
+            y = y.expand(it.count, 2, 3, 3).contiguous()
+            if rank == 0:
+                full[it.unit][it.first: it.first + it.count].copy_(y)
+            local[i] = y
+        dist.barrier()
+        for w in gather_to_root(items, local, full, rank):
+            w.wait()
+        if rank == 0:
+            results["full"] = {u: t.clone() for u, t in full.items()}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_to_root_gloo_world3():
+    """Every slab computed off rank 0 lands in place in rank 0's full outputs."""
+    world = 3
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_p2p_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    for u, b in enumerate([20, 5, 1, 3]):
+        want = (100.0 * u + torch.arange(b, dtype=torch.float32)).view(-1, 1, 1, 1).expand(b, 2, 3, 3)
+        assert torch.equal(results["full"][u], want)
+
+
+def test_bench_spawns_ranks_for_gpus_flag(monkeypatch):
+    """bench.py --gpus N without WORLD_SIZE re-launches itself under torch.distributed.run."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    monkeypatch.setattr(subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert e.value.code == 0
+    cmd = calls[0]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"] and "--nproc-per-node=4" in cmd
+    assert "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "2"]
