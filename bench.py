@@ -84,6 +84,9 @@ def parse_args(argv=None):
                     help="multi-GPU: shard = each unit's batch split across ranks + NCCL gather to rank 0 "
                          "(strong, north_star config 5); weak = every rank runs the sweep on its own images")
     ap.add_argument("--no-gather", action="store_true", help="shard mode: skip the output gather")
+    ap.add_argument("--groups", choices=("auto", "one", "batch"), default="auto",
+                    help="CUDA graphs per step: one (all ops concurrent), batch (one per batch size; the gather of "
+                         "a group overlaps the next group); auto = batch when gathering, else one")
     ap.add_argument("--per-op-out", default=None, help="write the per-op CSV here")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget (s)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -545,10 +548,12 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     # (NCCL p2p on NCCL's stream, overlapping the next group's compute)
     nstreams = max(1, args.streams)
     streams = [main] + [torch.cuda.Stream(device=dev) for _ in range(nstreams - 1)]
+    per_batch = args.groups == "batch" or (args.groups == "auto" and gather)
+    group_of = (lambda u: sweep[u][1].batch) if per_batch else (lambda u: 0)
     groups = []
-    for gb in sorted({s[1].batch for s in sweep}):
-        gitems = [it for it in items if sweep[it.unit][1].batch == gb]
-        idx = [i for i, r in enumerate(rows) if sweep[r[5].unit][1].batch == gb]
+    for gb in sorted({group_of(u) for u in range(len(sweep))}):
+        gitems = [it for it in items if group_of(it.unit) == gb]
+        idx = [i for i, r in enumerate(rows) if group_of(r[5].unit) == gb]
         local = {gitems.index(rows[i][5]): ops[i].y for i in idx}
         graph = capture([(ops[i], per_op[i]) for i in idx], streams) if idx else None
         groups.append((gb, graph, gitems, local))
@@ -743,10 +748,10 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
                    "parallelism": f"batch-shard x{world}" if world > 1 else "1 GPU",
                    "variant_source": "heuristic" if db is None else os.path.relpath(db_path, ROOT),
                    "l2": "working set ~0.6 GB > 126 MB L2 (no explicit flush)",
-                   "schedule": (f"{len(groups)} CUDA graphs per step (one per batch size), the ops of a graph on "
-                                f"{nstreams} concurrent branches (LPT by per-op time)"),
+                   "schedule": (f"{len(groups)} CUDA graph(s) per step" + (" (one per batch size)" if per_batch else "")
+                                + f", the ops of a graph on {nstreams} concurrent branches (LPT by per-op time)"),
                    "filter_pack_ms_once": round(pack_ms, 3),
-                   "group_ms": {str(g[0]): round(ms, 4) for g, ms in zip(groups, group_ms)},
+                   "group_ms": {("batch " + str(g[0]) if per_batch else "all"): round(ms, 4) for g, ms in zip(groups, group_ms)},
                    "per_batch_ms_isolated": {str(k): round(v[0], 4) for k, v in sorted(by_batch.items())},
                    "per_batch_tflops_isolated": {str(k): round(v[1] / v[0] / 1e9, 2) for k, v in sorted(by_batch.items())},
                    "serial_ms_per_step_rank0": round(sum(per_op), 4),

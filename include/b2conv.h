@@ -175,6 +175,11 @@ int64_t b2c_conv_bytes(const b2c_conv_desc* d);
 /* Number of kernel launches one b2c_conv_fwd issues for this (d, t). */
 int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t);
 
+/* CTAs of the main conv kernel b2c_conv_fwd launches for (d, t) (0 if inapplicable):
+ * with the runtime (the SM-time an op occupies) it is what a concurrent schedule of
+ * independent ops packs onto the 148 SMs. */
+int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t);
+
 /* Thread-local message for the last non-zero status. */
 const char* b2c_last_error(void);
 

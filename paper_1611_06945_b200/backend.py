@@ -39,6 +39,7 @@ EXPORTS = (
     "b2c_conv_flops",
     "b2c_conv_bytes",
     "b2c_conv_launches",
+    "b2c_conv_grid",
     "b2c_last_error",
     "b2c_version",
     "b2c_device_alloc",
@@ -102,6 +103,7 @@ def lib():
         L.b2c_conv_bytes.argtypes = [P(ConvDesc)]
         L.b2c_conv_bytes.restype = ctypes.c_int64
         L.b2c_conv_launches.argtypes = [P(ConvDesc), P(Tune)]
+        L.b2c_conv_grid.argtypes = [P(ConvDesc), P(Tune)]
         L.b2c_pool_max_fwd.argtypes = [P(PoolDesc), vp, vp, vp]
         L.b2c_relu_fwd.argtypes = [vp, vp, ctypes.c_int64, vp]
         L.b2c_xpose.argtypes = [P(XposeDesc), vp, vp, vp]

@@ -1053,6 +1053,29 @@ int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
 
 const char* b2c_last_error(void) { return g_last_error.c_str(); }
 
+int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t) {
+    std::string why;
+    if (applies_impl(d, t, why)) return 0;
+    const Geom g = make_geom(d);
+    switch (t->variant) {
+        case B2C_VAR_SIMPLE:
+            return (int)std::min<long long>(((long long)g.N * g.OC * g.PQ + 255) / 256, 148LL * 64);
+        case B2C_VAR_TILED: {
+            const int BM = t->mnb0 * t->mnt0, BN = t->mnb1 * t->mnt1;
+            return ((g.M + BM - 1) / BM) * ((g.OC + BN - 1) / BN);
+        }
+        case B2C_VAR_FC_STREAM:
+            return t->kb == 2 ? (g.OC + t->mnb0 * t->mnt1 - 1) / (t->mnb0 * t->mnt1) : (g.OC + t->mnt1 - 1) / t->mnt1;
+        default: {
+            const UmmaPlan p = umma_plan(d, t);
+            if (!t->tma) return p.grid_x * p.grid_y * p.split;
+            const int occ = t->stages == 2 ? 2 : 1, cl = t->cluster == 2 ? 2 : 1;
+            const int units = (cl == 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
+            return p.streamk ? p.sk_grid : cl == 2 ? 2 * std::min(units, num_sms() / 2) : std::min(units, occ * num_sms());
+        }
+    }
+}
+
 void* b2c_device_alloc(size_t bytes) {
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);

@@ -206,7 +206,8 @@ def candidates(node: OpNode, edges, space: TuneSpace | None = None, prec: int = 
 
 
 def sweep(node: OpNode, edges, space: TuneSpace | None = None, objective: str = WALL, reps: int = 5,
-          warmup: int = 2, l2_flush: bool = True, seed: str = "validate", jobs: int = 1, prec: int = 0) -> TuneRecord:
+          warmup: int = 2, l2_flush: bool = True, seed: str = "validate", jobs: int = 1, prec: int = 0,
+          record_all: list | None = None) -> TuneRecord:
     """Time every applicable candidate on the device and return the fastest one
     that matches the exact-order conv_simple output within tolerance.  Ties
     break by enumeration order (specialized variants first), tuner.py:367-373."""
@@ -245,6 +246,11 @@ def sweep(node: OpNode, edges, space: TuneSpace | None = None, objective: str = 
             failures.append(f"{v.name}[{params.to_string()}]: {e}")
             continue
         rec = TuneRecord(sig, v.name, params, round(ms * 1e6, 1), CostReport(wall_ns=int(ms * 1e6)), max_rel_err=err)
+        if record_all is not None:  # every valid candidate: (variant, params, ns, CTAs of the main kernel)
+            from . import backend
+
+            ctas = int(backend.lib().b2c_conv_grid(backend.ctypes.byref(op.plan.desc), backend.ctypes.byref(op.plan.tune)))
+            record_all.append((sig, v.name, params.to_string(), rec.cost, ctas))
         key = (rec.cost, idx)
         if best is None or key < best_key:
             best, best_key = rec, key

@@ -22,8 +22,8 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CASES = [(42, 20, "BN=128,sk=0,sw=0,dr=0,tm=1"), (38, 20, "BN=96,sk=4,sw=0,dr=0,tm=1"),
-         (2, 20, "BN=32,sk=2,sw=0,dr=0,tm=3"), (41, 20, "BN=64,sk=1,sw=0,dr=0,tm=4"),
+CASES = [(42, 20, "BN=128,sk=2,sw=0,dr=0,tm=1"), (38, 20, "BN=96,sk=4,sw=0,dr=0,tm=1"),
+         (4, 20, "BN=32,sk=2,sw=0,dr=0,tm=3"), (41, 20, "BN=64,sk=1,sw=0,dr=0,tm=4"),
          (25, 20, "BN=32,sk=4,sw=1,dr=0,tm=1"), (34, 5, "BN=96,sk=1,sw=0,dr=0,tm=1")]
 
 

@@ -30,19 +30,21 @@ def main():
     ap.add_argument("--rows", default=None, help="comma list of corpus rows (default all)")
     ap.add_argument("--merge", default=None, help="existing DB to merge into")
     ap.add_argument("--prec", type=int, default=0, help="0 fp32-exact, 1 bf16 mode")
+    ap.add_argument("--all-out", default=None, help="CSV of every valid candidate (sig, variant, params, ns, ctas)")
     ap.add_argument("--nets", default="alexnet,nin,googlenet_3a",
                     help="also tune the conv nodes of these network files (data/nets) at the same batches")
     args = ap.parse_args()
     db = tuner.load_db(args.merge) if args.merge and os.path.exists(args.merge) else tuner.TuneDB()
     rows = None if args.rows is None else {int(r) for r in args.rows.split(",")}
     t_all = time.time()
+    cand = [] if args.all_out else None
     for row, op in corpus.sweep_ops([int(b) for b in args.batches.split(",")]):
         if rows is not None and row not in rows:
             continue
         g = with_fused(op.graph(), "conv", "relu")
         node = g.node("conv")
         t0 = time.time()
-        rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2, prec=args.prec)
+        rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2, prec=args.prec, record_all=cand)
         db.add(rec)
         print(f"row{row:02d} N={op.batch:2d} {rec.op_signature:42s} {rec.variant:11s} {rec.params.to_string():60s} "
               f"{rec.cost / 1e3:9.2f} us  {op.flops_computed / rec.cost / 1e3:7.1f} TFLOP/s  err={rec.max_rel_err:.2e}  "
@@ -63,11 +65,16 @@ def main():
                 for node in g.nodes:
                     if node.kind != KIND_CONV or tuner.op_signature(node, g.edges) in db.records:
                         continue
-                    rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2, prec=args.prec)
+                    rec = tuner.sweep(node, g.edges, reps=args.reps, warmup=2, prec=args.prec, record_all=cand)
                     db.add(rec)
                     print(f"{net} N={b:2d} {rec.op_signature:42s} {rec.variant:11s} {rec.params.to_string():60s} "
                           f"{rec.cost / 1e3:9.2f} us", flush=True)
                 tuner.save_db(db, args.out)
+    if cand is not None:
+        with open(args.all_out, "w") as fh:
+            fh.write("signature,variant,params,ns,ctas\n")
+            for sig, vname, ps, ns, ctas in cand:
+                fh.write(f"{sig},{vname},\"{ps}\",{ns},{ctas}\n")
     print(f"tuned {len(db.records)} signatures in {time.time() - t_all:.0f}s -> {args.out}")
 
 
