@@ -76,9 +76,13 @@ def parse_args(argv=None):
     ap.add_argument("--prec", choices=("fp32", "bf16"), default="fp32",
                     help="fp32: fp32-exact (3xTF32 / FFMA, the headline); bf16: bf16 operands, fp32 accumulate "
                          "(separately stated tolerance rel 4e-3)")
-    ap.add_argument("--db", default=None, help="TuneDB path (default: shipped B200 DB of the precision)")
+    ap.add_argument("--db", default=None,
+                    help="latency TuneDB for the per-op runtimes (default: shipped B200 DB of the precision)")
+    ap.add_argument("--sweep-db", default=None,
+                    help="TuneDB for the concurrent step (default: the shipped *_sweep DB: per op the candidate "
+                         "minimising time x (CTAs/148)^0.5 within 3x of the fastest, tools/pick_db.py)")
     ap.add_argument("--heuristic", action="store_true", help="ignore the TuneDB, use select_variant's heuristic")
-    ap.add_argument("--streams", type=int, default=int(os.environ.get("B2C_BENCH_STREAMS", "4")),
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("B2C_BENCH_STREAMS", "16")),
                     help="concurrent graph branches the independent ops are spread over (1 = serial)")
     ap.add_argument("--mode", choices=("shard", "weak"), default="shard",
                     help="multi-GPU: shard = each unit's batch split across ranks + NCCL gather to rank 0 "
@@ -475,7 +479,11 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     prec = 1 if args.prec == "bf16" else 0
     db_path = args.db or tuner.shipped_db_path(args.prec)
     db = tuner.load_db(db_path) if (os.path.exists(db_path) and not args.heuristic) else None
-    sweep = build_sweep(batches, db, args.heuristic, prec)
+    sdb_path = args.sweep_db or tuner.shipped_db_path(args.prec + "_sweep")
+    sdb = tuner.load_db(sdb_path) if (os.path.exists(sdb_path) and not args.heuristic) else db
+    if sdb is db:
+        sdb_path = db_path
+    sweep = build_sweep(batches, sdb, args.heuristic, prec)  # the step's kernel choices
     shard_mode = world > 1 and args.mode == "shard"
     gather = shard_mode and not args.no_gather
 
@@ -493,37 +501,50 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
         for u, (row, op, node, edges, v, params) in enumerate(sweep):
             osz = edges[node.outputs[0]].sizes
             full_out[u] = torch.empty(tuple(osz), dtype=torch.float32, device=dev)
-    ops, hosts, rows = [], [], []
+    # ops: per-op runtimes (latency DB: one op at a time); sops: the step (sweep DB, concurrent);
+    # the same ConvOp where both DBs pick the same kernel and tile
+    ops, sops, sw_est, hosts, rows = [], [], [], [], []
     for it in items:
         if it.rank != rank:
             continue
         row, op, node, edges, v, params = sweep[it.unit]
         # weak mode: every rank its own images; shard mode: the slab of the unit's images
         x, f, b = make_inputs(op, node, edges, "" if shard_mode or rank == 0 else f":r{rank}")
-        if shard_mode and it.count != op.batch:  # a slab: the DB's choice for the slab's batch size
+        if shard_mode and it.count != op.batch:  # a slab: the DBs' choices for the slab's batch size
             op = op.with_batch(it.count)
             g = with_fused(op.graph(), "conv", "relu")
             node, edges = g.node("conv"), g.edges
-            v, params = select_variant(node, edges, None if args.heuristic else db, prec=prec)
+            v, params = select_variant(node, edges, None if args.heuristic else sdb, prec=prec)
             x = x[it.first: it.first + it.count]
+        vl, pl = select_variant(node, edges, None if args.heuristic else db, prec=prec)
+        sig = tuner.op_signature(node, edges)
         plan = v.generate(node, edges, params)
         dx, df, db_ = (torch.from_numpy(a.copy()).to(dev) for a in (x, f, b))
         y = full_out[it.unit][it.first: it.first + it.count] if it.unit in full_out else None
-        ops.append(runner.ConvOp(plan, dx, df, db_, y=y))
+        sop = runner.ConvOp(plan, dx, df, db_, y=y)
+        same = vl.name == v.name and pl.to_string() == params.to_string()
+        ops.append(sop if same else runner.ConvOp(vl.generate(node, edges, pl), dx, df, db_))
+        sops.append(sop)
+        rec = sdb.records.get(sig) if sdb is not None else None
+        sw_est.append(rec.cost * 1e-6 if rec is not None else op.flops_computed / 1e11)  # ms, for the LPT branches
         if not args.no_e2e:
             hosts.append(runner.HostRun.create(plan, x, f, b, device=dev))
-        rows.append((row, op, v.name, params, tuner.op_signature(node, edges), it))
+        rows.append((row, op, vl.name, pl, sig, it, v.name, params))
     torch.cuda.synchronize()
-    pack_ms = sum(o.prepare_ms() for o in ops)  # one-time filter packs (cached per filter tensor)
-    flops_mine = sum(conv_flops(o.plan.desc) for o in ops)
+    pack_ms = sum(o.prepare_ms() for o in sops)  # one-time filter packs (cached per filter tensor)
+    for o, so in zip(ops, sops):
+        if o is not so:
+            o.prepare()
+    flops_mine = sum(conv_flops(o.plan.desc) for o in sops)
     launches_mine = sum(int(be.lib().b2c_conv_launches(be.ctypes.byref(o.plan.desc), be.ctypes.byref(o.tune)))
-                        for o in ops)
+                        for o in sops)
+    n_same = sum(1 for o, so in zip(ops, sops) if o is so)
     tf32 = measure_tf32_peak(dev) if rank == 0 else None
 
     # ---- per-op isolated timing (the metric's "runtime per op"): serial graph, event between ops
     n = len(ops)
     main = torch.cuda.Stream(device=dev)
-    for o in ops:  # warm every kernel once (smem attributes, module load) outside capture
+    for o in ops + sops:  # warm every kernel once (smem attributes, module load) outside capture
         o.launch()
     torch.cuda.synchronize()
     per_op = [0.0] * n
@@ -554,8 +575,8 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     for gb in sorted({group_of(u) for u in range(len(sweep))}):
         gitems = [it for it in items if group_of(it.unit) == gb]
         idx = [i for i, r in enumerate(rows) if group_of(r[5].unit) == gb]
-        local = {gitems.index(rows[i][5]): ops[i].y for i in idx}
-        graph = capture([(ops[i], per_op[i]) for i in idx], streams) if idx else None
+        local = {gitems.index(rows[i][5]): sops[i].y for i in idx}
+        graph = capture([(sops[i], sw_est[i]) for i in idx], streams) if idx else None
         groups.append((gb, graph, gitems, local))
     torch.cuda.synchronize()
     if world > 1:
@@ -677,7 +698,7 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
             achieved = by / (t_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4)}
-        r_row, r_op, r_var, r_par, r_sig, _ = rows[dom]
+        r_row, r_op, r_var, r_par, r_sig = rows[dom][:5]
         roof.update({"traffic": None, "peak_source": peaks["source"], "tf32_measured_tflops": round(tf32, 1),
                      "kernel": f"{r_var} [{r_par.to_string()}]", "op": r_sig, "corpus_row": r_row,
                      "share_of_step": round(t_ms / sum(per_op), 4), "launch_ms": round(t_ms, 4),
@@ -692,18 +713,18 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
 
     # ---- per-op table (rank 0's items), configs 1-3 and 5
     per_rows = []
-    for i, (row, op, vname, params, sig, it) in enumerate(rows):
+    for i, (row, op, vname, params, sig, it) in enumerate(r[:6] for r in rows):
         fl_i, by_i = conv_flops(ops[i].plan.desc), conv_bytes(ops[i].plan.desc)
         per_rows.append([row, op.batch, round(per_op[i] * 1e3, 2), round(fl_i / per_op[i] / 1e9, 2),
                          round(frac_of_roof(fl_i, by_i, per_op[i]), 4)])
     if args.per_op_out:
         with open(args.per_op_out, "w") as fh:
-            fh.write("row,batch,signature,variant,params,ms,tflops,gbs,flops,bytes,frac_roofline\n")
-            for i, (row, op, vname, params, sig, it) in enumerate(rows):
+            fh.write("row,batch,signature,variant,params,ms,tflops,gbs,flops,bytes,frac_roofline,sweep_variant,sweep_params\n")
+            for i, (row, op, vname, params, sig, it, sv, sp) in enumerate(rows):
                 fl_i, by_i = conv_flops(ops[i].plan.desc), conv_bytes(ops[i].plan.desc)
                 fh.write(f"{row},{op.batch},{sig},{vname},\"{params.to_string()}\",{per_op[i]:.5f},"
                          f"{fl_i / per_op[i] / 1e9:.3f},{by_i / per_op[i] / 1e6:.1f},{fl_i},{by_i},"
-                         f"{frac_of_roof(fl_i, by_i, per_op[i]):.4f}\n")
+                         f"{frac_of_roof(fl_i, by_i, per_op[i]):.4f},{sv},\"{sp.to_string()}\"\n")
 
     def subset(pred):
         idx = [i for i, r in enumerate(rows) if pred(r[0], sweep[r[5].unit][1].batch)]
@@ -726,7 +747,7 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     if not args.no_cpu and world == 1:
         cpu = cpu_baseline(batches, args.cpu_seconds)
     by_batch = {}
-    for i, (row, op, vname, params, sig, it) in enumerate(rows):
+    for i, (row, op, vname, params, sig, it) in enumerate(r[:6] for r in rows):
         e = by_batch.setdefault(sweep[it.unit][1].batch, [0.0, 0])
         e[0] += per_op[i]
         e[1] += conv_flops(ops[i].plan.desc)
@@ -746,7 +767,9 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
                                      "next group; inside the timed step" if gather else "none"),
                    "ops_per_step": len(sweep), "launches_rank0": n, "flops_per_step": int(flops_all),
                    "parallelism": f"batch-shard x{world}" if world > 1 else "1 GPU",
-                   "variant_source": "heuristic" if db is None else os.path.relpath(db_path, ROOT),
+                   "variant_source": "heuristic" if db is None else
+                   {"per_op": os.path.relpath(db_path, ROOT), "step": os.path.relpath(sdb_path, ROOT),
+                    "ops_with_same_choice": n_same},
                    "l2": "working set ~0.6 GB > 126 MB L2 (no explicit flush)",
                    "schedule": (f"{len(groups)} CUDA graph(s) per step" + (" (one per batch size)" if per_batch else "")
                                 + f", the ops of a graph on {nstreams} concurrent branches (LPT by per-op time)"),

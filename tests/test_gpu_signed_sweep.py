@@ -1,6 +1,6 @@
 """Signed-input parity of the production configuration: all 129 sweep ops (43
 corpus rows x N = 1/5/20) on U[-1, 1) operands, each on the kernel and tile the
-SHIPPED TuneDB selects (fp32 DB, then the bf16 DB), two seeds.
+SHIPPED TuneDBs select (the latency and the sweep DB of each precision), two seeds.
 
 The reference's own data (U[0.1, 1), cuclgen/oracle.py:53-60) makes every
 conv output positive, so ReLU never clips on it (SURVEY.md §8(c) caveat; the
@@ -26,12 +26,12 @@ pytestmark = pytest.mark.gpu
 SEEDS = ("signed-a", "signed-b")
 
 
-def _sweep_choices(prec):
+def _sweep_choices(dbname, prec):
     from paper_1611_06945_b200 import corpus, tuner
     from paper_1611_06945_b200.frontend import with_fused
     from paper_1611_06945_b200.variants import select_variant
 
-    db = tuner.load_db(tuner.shipped_db_path("bf16" if prec else "fp32"))
+    db = tuner.load_db(tuner.shipped_db_path(dbname))
     out = []
     for row, op in corpus.sweep_ops([1, 5, 20]):
         g = with_fused(op.graph(), "conv", "relu")
@@ -44,15 +44,22 @@ def _sweep_choices(prec):
     return out
 
 
-@pytest.mark.parametrize("prec", [0, 1], ids=["fp32_db", "bf16_db"])
-def test_sweep_signed_inputs_shipped_db(cuda, prec):
+@pytest.mark.parametrize("dbname", ["fp32", "fp32_sweep", "bf16", "bf16_sweep"])
+def test_sweep_signed_inputs_shipped_db(cuda, dbname):
     import torch
 
     from paper_1611_06945_b200 import runner
 
+    import os
+
+    from paper_1611_06945_b200 import tuner
+
+    if not os.path.exists(tuner.shipped_db_path(dbname)):
+        pytest.fail(f"shipped DB {dbname} missing")
+    prec = 1 if dbname.startswith("bf16") else 0
     k = 8e-3 if prec else 1e-5
     failures, clipped_total, variants_seen = [], 0, set()
-    for row, op, node, edges, v, p in _sweep_choices(prec):
+    for row, op, node, edges, v, p in _sweep_choices(dbname, prec):
         plan = v.generate(node, edges, p)
         variants_seen.add((v.name, p.tma, p.split_k != 1))
         for seed in SEEDS:
