@@ -110,6 +110,10 @@ typedef struct b2c_tune {
                         rows, x start rounded down to 16 bytes; input width a multiple of 4) */
     int32_t cluster; /* TMA kernel: 2 = CTA pairs (thread-block clusters) take neighbouring pixel tiles of the
                         same filter tile and multicast each filter stage to both (half the filter L2 traffic);
+                        3 = 2-SM UMMA pairs: the same two pixel tiles as ONE tcgen05.mma.cta_group::2 of
+                        M = 256 issued by the leader CTA, each CTA holding half of the filter tile's rows
+                        (half the filter L2 and shared-memory traffic per CTA; tile_n 64 | 128 | 192,
+                        fp32-exact mode, tma 1 | 3 | 4);
                         0/1 = single CTAs.  Pairs need swap_ab = 0 and a conv (not fc) variant. */
 } b2c_tune;
 

@@ -119,7 +119,7 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
         if (t->variant != B2C_VAR_UMMA && t->variant != B2C_VAR_1X1) {
             why = "bf16 mode: tcgen05 conv_umma / conv_1x1 only"; return B2C_INAPPLICABLE;
         }
-        if (!t->tma || t->swap_ab || t->cluster == 2 || t->stages == 2 || (t->tma == 2 && d->c <= 4)) {
+        if (!t->tma || t->swap_ab || t->cluster >= 2 || t->stages == 2 || (t->tma == 2 && d->c <= 4)) {
             why = "bf16 mode: TMA kernel (tma=1|2), swap_ab=0, single CTAs, not the 8-tap first-layer path";
             return B2C_INAPPLICABLE;
         }
@@ -177,7 +177,8 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     // tcgen05 family
     if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192"; return B2C_INAPPLICABLE; }
     if (t->split_k < 0 || (t->split_k == 0 && !t->tma)) { why = "split_k must be >= 1 (0 = stream-K, TMA kernel only)"; return B2C_BAD_ARGS; }
-    if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K is single-CTA"; return B2C_INAPPLICABLE; }
+    if (t->cluster < 0 || t->cluster > 3) { why = "cluster must be 0..3"; return B2C_BAD_ARGS; }
+    if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K: single CTAs or 2-SM pairs"; return B2C_INAPPLICABLE; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
     if (t->tma < 0 || t->tma > 4) { why = "tma must be 0..4"; return B2C_BAD_ARGS; }
@@ -185,7 +186,7 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
         if (d->stride != 1 || d->r < 2 || t->variant == B2C_VAR_FC) {
             why = "tma=4 (direct NCHW k x k) needs a stride-1 conv with ksz >= 2"; return B2C_INAPPLICABLE;
         }
-        if (t->swap_ab || t->cluster == 2) { why = "tma=4: pixels on M (swap_ab=0), single CTAs"; return B2C_INAPPLICABLE; }
+        if (t->swap_ab || t->cluster == 2) { why = "tma=4: pixels on M (swap_ab=0), no multicast pairs"; return B2C_INAPPLICABLE; }
         if (d->w % 4 || d->ow + 3 > UMMA_M) {
             why = "tma=4: input width must be a multiple of 4 (16-byte TMA rows) and ow <= 125"; return B2C_INAPPLICABLE;
         }
@@ -194,7 +195,7 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
         if (!(d->r == 1 && d->stride == 1 && d->pad == 0) || t->variant == B2C_VAR_FC) {
             why = "tma=3 (direct NCHW) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
         }
-        if (t->swap_ab || t->cluster == 2) { why = "tma=3: pixels on M (swap_ab=0), single CTAs"; return B2C_INAPPLICABLE; }
+        if (t->swap_ab || t->cluster == 2) { why = "tma=3: pixels on M (swap_ab=0), no multicast pairs"; return B2C_INAPPLICABLE; }
         if (((long long)d->h * d->w * 4) % 16) { why = "tma=3: h*w*4 bytes must be a multiple of 16 (TMA strides)"; return B2C_INAPPLICABLE; }
     }
     if (t->tma && t->stages == 2 && t->tile_n > 64) { why = "two CTAs per SM (stages=2) need tile_n <= 64"; return B2C_INAPPLICABLE; }
@@ -203,6 +204,15 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
         return B2C_INAPPLICABLE;
     }
     if (t->cluster == 2 && t->tma == 2 && d->c <= 4) { why = "CTA pairs: not with the 8-tap first-layer path"; return B2C_INAPPLICABLE; }
+    if (t->cluster == 3) {  // 2-SM UMMA (tcgen05 cta_group::2, M = 256)
+        if (!t->tma || t->swap_ab || t->variant == B2C_VAR_FC || t->tile_n < 64 || t->stages == 2) {
+            why = "2-SM UMMA pairs (cluster=3) need the TMA kernel, swap_ab=0, a conv variant, tile_n >= 64, 1 CTA/SM";
+            return B2C_INAPPLICABLE;
+        }
+        if (t->tma == 2) { why = "2-SM UMMA pairs: not with tma=2 (2-D tiles / 8-tap first-layer boxes)"; return B2C_INAPPLICABLE; }
+        if (t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) { why = "2-SM UMMA pairs: tile_n in {64, 128, 192}"; return B2C_INAPPLICABLE; }
+        if (d->prec != B2C_PREC_FP32) { why = "2-SM UMMA pairs: fp32-exact mode only"; return B2C_INAPPLICABLE; }
+    }
     if (t->tma == 2 && !(d->r == 1 && d->stride == 1 && d->pad == 0) && t->variant != B2C_VAR_FC && d->c > 4) {
         why = "tma=2 (2-D tiled pixels) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
     }
@@ -292,9 +302,13 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.sk_grid = p.sk_maxc = 0;
     size_t nslots = p.split > 1 ? (size_t)p.tiles * p.split : 0;
     if (p.streamk) {
-        const long long W = (long long)p.tiles * p.kblocks;
-        p.sk_grid = (int)std::min<long long>(W, num_sms());
-        const long long L = std::max<long long>(1, W / p.sk_grid);  // K blocks per CTA (floor)
+        // 2-SM pairs share units (two neighbouring pixel tiles): stream-K over pair-units, one share per pair
+        const bool pair = t->cluster == 3;
+        const long long units = pair ? (long long)((p.grid_x + 1) / 2) * p.grid_y : p.tiles;
+        const long long W = units * p.kblocks;
+        const int ctas = (int)std::min<long long>(W, pair ? num_sms() / 2 : num_sms());  // CTAs (pairs)
+        p.sk_grid = pair ? 2 * ctas : ctas;
+        const long long L = std::max<long long>(1, W / ctas);  // K blocks per CTA / pair (floor)
         p.sk_maxc = (int)((p.kblocks + L - 1) / L + 1);
         nslots = (size_t)p.tiles * p.sk_maxc;
     }
@@ -566,6 +580,16 @@ TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
         }
         return TconvEntry{nullptr, 0, 0};
     }
+    if (cl == 3) {  // 2-SM UMMA pairs
+        if constexpr (!SWAP && MODE != 1 && MODE != 2 && MODE != 3) {
+            switch (bn) {
+                case 64: return tconv_entry<64, false, MODE, 1, 3>();
+                case 128: return tconv_entry<128, false, MODE, 1, 3>();
+                case 192: return tconv_entry<192, false, MODE, 1, 3>();
+            }
+        }
+        return TconvEntry{nullptr, 0, 0};
+    }
     if (occ == 2) {
         switch (bn) {
             case 32: return tconv_entry<32, SWAP, MODE, 2, 1>();
@@ -619,7 +643,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
     const int mode = t->tma == 4 ? 6 : t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
-    const int cl = t->cluster == 2 ? 2 : 1;
+    const int cl = (t->cluster == 2 || t->cluster == 3) ? t->cluster : 1;
     TconvEntry e{nullptr, 0, 0};
     if (d->prec == B2C_PREC_BF16)
         e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
@@ -709,7 +733,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.tiles_n = p.grid_y;
     a.tiles_m = p.grid_x;
     // CL = 2: units are pair-units (two neighbouring pixel tiles)
-    a.units = (cl == 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
+    a.units = (cl >= 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
     a.bx = p.bx;
     a.by = p.by;
     a.tiles_x = p.tiles_x;
@@ -745,9 +769,9 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         if (no_skip) a.ksteps_last = TM_BK / 8;
     }
     const int grid = p.streamk ? p.sk_grid
-                     : cl == 2  ? 2 * std::min(a.units, num_sms() / 2)
+                     : cl >= 2  ? 2 * std::min(a.units, num_sms() / 2)
                                 : std::min(a.units, occ * num_sms());
-    cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, cl, tm_pix, tm_flt, a);
+    cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, cl >= 2 ? 2 : 1, tm_pix, tm_flt, a);
     if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
     return B2C_OK;
 }
@@ -1069,7 +1093,7 @@ int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t) {
         default: {
             const UmmaPlan p = umma_plan(d, t);
             if (!t->tma) return p.grid_x * p.grid_y * p.split;
-            const int occ = t->stages == 2 ? 2 : 1, cl = t->cluster == 2 ? 2 : 1;
+            const int occ = t->stages == 2 ? 2 : 1, cl = t->cluster >= 2 ? 2 : 1;
             const int units = (cl == 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
             return p.streamk ? p.sk_grid : cl == 2 ? 2 * std::min(units, num_sms() / 2) : std::min(units, occ * num_sms());
         }

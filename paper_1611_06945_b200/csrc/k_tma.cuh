@@ -76,11 +76,17 @@ constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 // PREC 1: bf16 operands, fp32 accumulate (kind::f16): the split warps round the fp32
 //         pixel tile to bf16 into TMEM; filters are packed once as bf16 in the
 //         no-swizzle core-matrix layout [8-element chunk][rows][16 B].
+// CL: 1 single CTAs; 2 CTA pairs (clusters of 2) multicasting each filter stage to both,
+// each CTA issuing its own M = 128 MMAs; 3 2-SM UMMA pairs (tcgen05 cta_group::2): the
+// leader issues M = 256 MMAs over both CTAs' pixel tiles, each CTA holding half of the
+// filter tile (B rows) and its own 128 accumulator rows.
 template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
     static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && CL == 1), "bf16: pixels on M, packed filters");
-    static_assert((MODE != 5 && MODE != 6) || CL == 1, "MODE 5/6: single CTAs");
-    static_assert(CL == 1 || (CL == 2 && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
+    static_assert((MODE != 5 && MODE != 6) || CL != 2, "MODE 5/6: no multicast pairs");
+    static_assert(CL == 1 || ((CL == 2 || CL == 3) && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
+    static constexpr bool PAIR = CL == 3;  // 2-SM UMMA
+    static_assert(!PAIR || (BN >= 64 && BN <= 192), "2-SM UMMA: N = BN in [64, 192] (two accumulators + A slots in TMEM)");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
     // drain warp groups (column halves); two groups halve the exposed epilogue
@@ -98,11 +104,13 @@ struct TmaCfg {
     static constexpr bool A_PRESPLIT = false;
     static constexpr bool B_SPLIT = SWAP || MODE == 1;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
-    static constexpr int B_BYTES = PREC ? BN * 64 : 2 * BN * 128;  // bf16 | raw + lo
+    static constexpr int B_BYTES = PREC ? BN * 64 : (PAIR ? 1 : 2) * BN * 128;  // bf16 | raw + lo (a pair: half the rows each)
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
     static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
     static constexpr int FLT_STAGE = PREC ? FLT_ROWS * 64 : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
+    static constexpr int FLT_HALF = FLT_ROWS / 2 * 128;   // 2-SM pair: one CTA's rows of one (raw | lo) image
+    static constexpr int FLT_CTA = PAIR ? 2 * FLT_HALF : FLT_STAGE;  // filter bytes landing in one CTA per K block
     static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
     // OCC CTAs per SM share its 228 KB of shared memory (1 KB per CTA is the driver's) and 512 TMEM columns
     static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024;
@@ -117,7 +125,10 @@ struct TmaCfg {
     static constexpr int A_SLOTS = A_SLOTS_FIT < 4 ? A_SLOTS_FIT : 4;
     static_assert(ACC_COLS + A_SLOTS * 64 <= TMEM_COLS, "TMEM budget");
     static constexpr bool SW128 = MODE != 3;
-    static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_STAGE);
+    static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_CTA);
+    // barrier arrival counts (a pair's leader counts its peer's split / drain warps too)
+    static constexpr int SPLIT_ARRIVALS = PAIR ? 2 * (TM_SPLIT_THREADS / 32) : TM_SPLIT_THREADS;
+    static constexpr int DRAIN_ARRIVALS = PAIR ? 2 * (DRAIN_THREADS / 32) : DRAIN_THREADS;
     static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
     static_assert((MODE != 5 && MODE != 6) || !SWAP, "MODE 5/6 tiles are pixel blocks on M (split warps transpose them)");
     static_assert(STAGES >= 2, "need at least two stages");
@@ -168,13 +179,19 @@ struct UnitCursor {
 
 __device__ __forceinline__ long long sk_start(long long W, int G, int c) { return (long long)c * W / G; }
 
+// Stream-K shares go to CTAs, or to CTA pairs (CL >= 2: both CTAs of a pair walk the same pair-units).
+template <int CL>
+__device__ __forceinline__ int sk_ctas() { return (int)gridDim.x / (CL >= 2 ? 2 : 1); }
+template <int CL>
+__device__ __forceinline__ int sk_me() { return (int)blockIdx.x / (CL >= 2 ? 2 : 1); }
+
 template <int PIX_ROWS, int FLT_ROWS, int MODE, int CL>
 __device__ __forceinline__ UnitCursor cursor_begin(const TArgs& a, int ubase) {
     UnitCursor c;
     c.u = ubase;
     const long long W = (long long)a.units * a.kblocks;
-    c.k = sk_start(W, gridDim.x, blockIdx.x);
-    c.end = sk_start(W, gridDim.x, blockIdx.x + 1);
+    c.k = sk_start(W, sk_ctas<CL>(), sk_me<CL>());
+    c.end = sk_start(W, sk_ctas<CL>(), sk_me<CL>() + 1);
     return c;
 }
 
@@ -193,7 +210,7 @@ __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     w.z = u % a.split;
     const int t2 = u / a.split;
     const int nt = t2 % a.tiles_n;
-    const int mt = CL == 2 ? 2 * (t2 / a.tiles_n) + rank : t2 / a.tiles_n;
+    const int mt = CL >= 2 ? 2 * (t2 / a.tiles_n) + rank : t2 / a.tiles_n;
     w.ghost = mt >= a.tiles_m;
     w.t = mt * a.tiles_n + nt;
     w.m0 = mt * PIX_ROWS;
@@ -227,7 +244,7 @@ __device__ __forceinline__ bool next_unit(const TArgs& a, UnitCursor& cur, int u
         w.nkb = n;
         // CTAs owning this unit's first and last K block
         const long long W = (long long)a.units * a.kblocks;
-        const int G = gridDim.x;
+        const int G = sk_ctas<CL>();
         const long long x0 = (long long)u * a.kblocks, x1 = x0 + a.kblocks - 1;
         int c0 = (int)(x0 * G / W), c1 = (int)(x1 * G / W);
         while (c0 + 1 < G && sk_start(W, G, c0 + 1) <= x0) ++c0;
@@ -235,7 +252,7 @@ __device__ __forceinline__ bool next_unit(const TArgs& a, UnitCursor& cur, int u
         while (c1 + 1 < G && sk_start(W, G, c1 + 1) <= x1) ++c1;
         while (c1 > 0 && sk_start(W, G, c1) > x1) --c1;
         w.nsplit = c1 - c0 + 1;
-        w.z = (int)blockIdx.x - c0;
+        w.z = sk_me<CL>() - c0;
         w.pslot0 = w.t * a.sk_maxc;
         cur.k += n;
         return true;
@@ -384,7 +401,11 @@ __device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
 // pair, each CTA fetches half (raw | lo) and multicasts it to both.
 template <int BYTES, int CL>
 __device__ __forceinline__ void load_filters(uint32_t dst, const char* src, uint32_t bar, int rank) {
-    if (CL == 2) {
+    if (CL == 3) {  // 2-SM pair: this CTA's half of the rows of the raw image and of the lo image
+        constexpr uint32_t H = BYTES / 4;
+        bulk_g2s(dst, src + (size_t)rank * H, H, bar);
+        bulk_g2s(dst + H, src + BYTES / 2 + (size_t)rank * H, H, bar);
+    } else if (CL == 2) {
         constexpr uint32_t H = BYTES / 2;
         bulk_g2s_mc(dst + (uint32_t)rank * H, src + (size_t)rank * H, H, bar, (uint16_t)0x3);
     } else {
@@ -641,31 +662,37 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int G = a.drain;
-    const int rank = CL == 2 ? (int)cluster_ctarank() : 0;
-    const int ubase = (int)blockIdx.x / CL, ustride = (int)gridDim.x / CL;
+    const int rank = CL >= 2 ? (int)cluster_ctarank() : 0;
+    constexpr int NCTA = CL >= 2 ? 2 : 1;  // CTAs per cluster
+    const int ubase = (int)blockIdx.x / NCTA, ustride = (int)gridDim.x / NCTA;
     if (tid == 0) B2C_TRACE(a.trace, 0);
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&raw_full[s]), 1);
-            mbar_init(smem_u32(&split_full[s]), TM_SPLIT_THREADS);
-            mbar_init(smem_u32(&empty_bar[s]), CL);  // one tcgen05.commit per CTA of the pair
+            mbar_init(smem_u32(&split_full[s]), Cfg::SPLIT_ARRIVALS);
+            mbar_init(smem_u32(&empty_bar[s]), CL == 2 ? 2 : 1);  // one tcgen05.commit per MMA-issuing CTA
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull_bar[s]), 1);
-            mbar_init(smem_u32(&tempty_bar[s]), Cfg::DRAIN_THREADS);
+            mbar_init(smem_u32(&tempty_bar[s]), Cfg::DRAIN_ARRIVALS);
         }
         for (int s = 0; s < Cfg::A_SLOTS; ++s) mbar_init(smem_u32(&afree_bar[s]), 1);
         mbar_fence_init();
     }
-    if (warp == Cfg::MMA_WARP) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    if (warp == Cfg::MMA_WARP) {
+        if (Cfg::PAIR)
+            tmem_alloc_pair(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+        else
+            tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    }
     if (warp == Cfg::LOAD_WARP && lane == 0) {
         tma_prefetch_desc(&tm_pix);
         if (MODE == 1) tma_prefetch_desc(&tm_flt);
     }
     tc_fence_before();
     __syncthreads();
-    if (CL == 2) cluster_sync_all();  // the peer's barriers exist before any multicast reaches them
+    if (CL >= 2) cluster_sync_all();  // the peer's barriers exist before any multicast / remote arrive reaches them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (tid == 0) B2C_TRACE(a.trace, 1);
@@ -714,7 +741,14 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 fence_proxy_async_smem();
                 tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(smem_u32(&split_full[stage]));
+                if (Cfg::PAIR) {  // one arrive per warp on the leader's barrier (relaxed: a release at
+                    // cluster scope costs ~1.5k cycles per stage and paced the whole pipeline; the TMEM
+                    // stores are complete at tcgen05.wait::st and the smem operand was written by TMA)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster_relaxed(smem_u32(&split_full[stage]), 0);
+                } else {
+                    mbar_arrive(smem_u32(&split_full[stage]));
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1u;
@@ -745,7 +779,12 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 tc_fence_after();
                 tmem_add_cols<DC>(t_row + (uint32_t)(slot * BN), acc);
                 tc_fence_before();
-                mbar_arrive(smem_u32(&tempty_bar[slot]));
+                if (Cfg::PAIR) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster_relaxed(smem_u32(&tempty_bar[slot]), 0);
+                } else {
+                    mbar_arrive(smem_u32(&tempty_bar[slot]));
+                }
             }
             if (dtid == 0 && ui == 0) B2C_TRACE(a.trace, 4);
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 208 + 2 * ui);
@@ -755,9 +794,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
             ++ui;
         }
         if (dtid == 0) B2C_TRACE(a.trace, 6);
-    } else if (warp == Cfg::MMA_WARP) {
+    } else if (warp == Cfg::MMA_WARP && (!Cfg::PAIR || rank == 0)) {
         // ------------------------------------------------------------ MMA issuer (whole warp waits, one lane issues)
-        constexpr uint32_t idesc = umma_idesc(PREC == 1 ? 1 : 2, TM_M, BN);
+        constexpr uint32_t idesc = umma_idesc(PREC == 1 ? 1 : 2, Cfg::PAIR ? 2 * TM_M : TM_M, BN);
         int stage = 0, cidx = 0, n = 0;
         uint32_t phase = 0;
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
@@ -771,19 +810,25 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 const bool first = kin == 0;
                 const bool last = (kin == G - 1) || (i == w.nkb - 1);
                 if (first && cidx >= 2) {
-                    mbar_wait(smem_u32(&tempty_bar[slot]), (uint32_t)((cidx >> 1) - 1) & 1u);
+                    if (Cfg::PAIR)
+                        mbar_wait_cluster(smem_u32(&tempty_bar[slot]), (uint32_t)((cidx >> 1) - 1) & 1u);
+                    else
+                        mbar_wait(smem_u32(&tempty_bar[slot]), (uint32_t)((cidx >> 1) - 1) & 1u);
                     tc_fence_after();
                 }
                 // split_full is armed only after the split threads observed
-                // raw_full, so it also covers the TMA / bulk bytes.
-                mbar_wait(smem_u32(&split_full[stage]), phase);
+                // raw_full, so it also covers the TMA / bulk bytes (a pair: both CTAs').
+                if (Cfg::PAIR)
+                    mbar_wait_cluster(smem_u32(&split_full[stage]), phase);
+                else
+                    mbar_wait(smem_u32(&split_full[stage]), phase);
                 tc_fence_after();
                 if (lane == 0 && n < 32) B2C_TRACE(a.trace, 112 + n);
                 if (elect_one_sync()) {
                     const uint32_t a_hi = tmem_base + (uint32_t)(Cfg::ACC_COLS + (n % Cfg::A_SLOTS) * 64);
                     const uint32_t a_lo = a_hi + 32;
                     const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
-                    const uint32_t b_lo = b_raw + BN * 128;
+                    const uint32_t b_lo = b_raw + (Cfg::PAIR ? BN / 2 : BN) * 128;
                     const uint32_t d = tmem_base + (uint32_t)(slot * BN);
                     if constexpr (PREC == 1) {  // bf16: two K=16 MMAs per 32-wide K block
 #pragma unroll
@@ -804,19 +849,33 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                             dbh = umma_desc(b_raw + s * 2 * BN * 16, BN * 16, 128);
                             dbl = umma_desc(b_lo + s * 2 * BN * 16, BN * 16, 128);
                         }
+                        if constexpr (Cfg::PAIR) {
+                            mma_tf32_ts_pair(d, a_hi + 8 * s, dbh, idesc, (first && s == 0) ? 0u : 1u);
+                            if (!(a.trace & 2)) {
+                                mma_tf32_ts_pair(d, a_hi + 8 * s, dbl, idesc, 1u);
+                                mma_tf32_ts_pair(d, a_lo + 8 * s, dbh, idesc, 1u);
+                            }
+                        } else {
                         mma_tf32_ts(d, a_hi + 8 * s, dbh, idesc, (first && s == 0) ? 0u : 1u);
                         if (!(a.trace & 2)) {  // debug bit 1: hi*hi only (timing experiments only)
                             mma_tf32_ts(d, a_hi + 8 * s, dbl, idesc, 1u);
                             mma_tf32_ts(d, a_lo + 8 * s, dbh, idesc, 1u);
                         }
+                        }
                     }
                     }
+                    if (Cfg::PAIR) {  // both CTAs' stage, A slot and accumulator slot
+                        tc_commit_pair(smem_u32(&empty_bar[stage]), (uint16_t)0x3);
+                        tc_commit_pair(smem_u32(&afree_bar[n % Cfg::A_SLOTS]), (uint16_t)0x3);
+                        if (last) tc_commit_pair(smem_u32(&tfull_bar[slot]), (uint16_t)0x3);
+                    } else {
                     if (CL == 2)  // the stage's filter half may be refilled by either CTA
                         tc_commit_mc(smem_u32(&empty_bar[stage]), (uint16_t)0x3);
                     else
                         tc_commit(smem_u32(&empty_bar[stage]));
                     tc_commit(smem_u32(&afree_bar[n % Cfg::A_SLOTS]));
                     if (last) tc_commit(smem_u32(&tfull_bar[slot]));
+                    }
                     if (n < 32) B2C_TRACE(a.trace, 144 + n);
                 }
                 __syncwarp();
@@ -833,7 +892,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
             }
         }
         if (lane == 0) B2C_TRACE(a.trace, 5);
-    } else if (lane == 0) {
+    } else if (warp == Cfg::LOAD_WARP && lane == 0) {
         // ------------------------------------------------------------ TMA / bulk loader
         int stage = 0, n = 0;
         uint32_t phase = 0;
@@ -847,12 +906,14 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                                     ((size_t)(w0.n0 / Cfg::FLT_ROWS) * a.kblocks + w0.kb_begin) * (size_t)Cfg::FLT_STAGE;
                 for (int i = 0; i < npre; ++i) {
                     const uint32_t bar = smem_u32(&raw_full[i]);
-                    mbar_expect_tx(bar, Cfg::FLT_STAGE);
+                    mbar_expect_tx(bar, Cfg::FLT_CTA);
                     load_filters<Cfg::FLT_STAGE, CL>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
                                                     wsrc0 + (size_t)i * Cfg::FLT_STAGE, bar, rank);
                 }
             }
+            B2C_TRACE(a.trace, 8);
             pdl_wait();
+            B2C_TRACE(a.trace, 9);
         }
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
         for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
@@ -879,7 +940,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 const uint32_t bytes = (MODE == 4   ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u
                                         : MODE == 6 ? Cfg::BYTES - (uint32_t)(TM_M - a.box_w * a.by) * 128u
                                                     : Cfg::BYTES) -
-                                       (pre ? (uint32_t)Cfg::FLT_STAGE : 0u);
+                                       (pre ? (uint32_t)Cfg::FLT_CTA : 0u);
                 mbar_arrive_expect_tx(bar, bytes);
                 if (n < 32) B2C_TRACE(a.trace, 176 + n);
                 if (MODE == 1) {
@@ -931,10 +992,13 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     }
     if (tid == 0) B2C_TRACE(a.trace, 2);
     __syncthreads();
-    if (CL == 2) cluster_sync_all();  // no multicast or remote commit may still target this CTA
+    if (CL >= 2) cluster_sync_all();  // no multicast or remote commit may still target this CTA
     if (warp == Cfg::MMA_WARP) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+        if (Cfg::PAIR)
+            tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+        else
+            tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }
     if (tid == 0) B2C_TRACE(a.trace, 7);
 }

@@ -63,7 +63,11 @@ def _variant_params(g):
                     TuneParams(bn=96, split_k=2, tma=2, cl=2), TuneParams(bn=32, tma=3), TuneParams(bn=128, tma=3),
                     TuneParams(bn=64, split_k=2, tma=3), TuneParams(bn=96, split_k=0, tma=3), TuneParams(bn=64, tma=3, occ=2),
                     TuneParams(bn=32, tma=4), TuneParams(bn=128, split_k=2, tma=4), TuneParams(bn=64, split_k=0, tma=4),
-                    TuneParams(bn=64, tma=4, occ=2)):
+                    TuneParams(bn=64, tma=4, occ=2), TuneParams(bn=64, tma=1, cl=3),
+                    TuneParams(bn=128, split_k=2, tma=1, cl=3), TuneParams(bn=192, tma=1, cl=3),
+                    TuneParams(bn=128, tma=4, cl=3), TuneParams(bn=64, split_k=2, tma=3, cl=3),
+                    TuneParams(bn=128, tma=3, cl=3), TuneParams(bn=128, split_k=0, tma=1, cl=3),
+                    TuneParams(bn=64, split_k=0, tma=4, cl=3)):
             out.append((v, prm))
     out += [("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)),
             ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1)),

@@ -1,0 +1,11 @@
+#!/bin/bash
+OUT=gpurun_out/r2n; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k golden > $OUT/pytest_golden.log 2>&1; echo "exit $?" >> $OUT/pytest_golden.log
+tail -2 $OUT/pytest_golden.log
+P="BN=128,sk=0,tm=1 BN=128,sk=1,tm=1,cl=3 BN=128,sk=0,tm=1,cl=3 BN=192,sk=0,tm=1,cl=3 BN=64,sk=0,tm=1,cl=3"
+timeout 300 python tools/try_params.py --ops 42:20,40:20,37:20,38:20,39:20,36:20,42:5,40:5 --params $P > $OUT/try.log 2>&1
+cat $OUT/try.log
+P4="BN=192,sk=1,tm=4 BN=192,sk=1,tm=4,cl=3 BN=128,sk=0,tm=4,cl=3 BN=192,sk=0,tm=4,cl=3"
+timeout 300 python tools/try_params.py --ops 41:20,31:20,41:5 --params $P4 > $OUT/try4.log 2>&1
+cat $OUT/try4.log
