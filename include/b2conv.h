@@ -60,6 +60,11 @@ extern "C" {
 #define B2C_VAR_1X1 2    /* "conv_1x1"   : k=1,pad=0 tcgen05 GEMM                     (variants.py:279-325) */
 #define B2C_VAR_FC 3     /* "conv_fc"    : whole-image filter, weight-streaming GEMM  (variants.py:328-373) */
 #define B2C_VAR_UMMA 4   /* "conv_umma"  : tcgen05/TMEM 3xTF32 implicit GEMM, k x k      (new, B200)       */
+#define B2C_VAR_WINO 6   /* "conv_wino"  : Winograd F(2x2,3x3) for 3x3 / stride-1 / pad <= 1 convs, fp32-exact:
+                              input transform V = B^T d B, 16 batched tcgen05 3xTF32 GEMMs against the
+                              filter transform U = G g G^T (made by b2c_conv_prepare), output transform
+                              A^T M A + bias + ReLU (the paper's gap to cuDNN on 3x3).
+                              tile_n 64|128|192, split_k (0 = stream-K), swap_ab; 3 launches */
 #define B2C_VAR_FC_STREAM 5 /* "conv_fc_stream": fp32 FFMA weight streaming for ConvFC (HBM-bound at small
                               batch; reads w once).  kb = 1 (batch <= 8): warps split K, mnb0 = warps per
                               block 2|4|8, mnt1 = rows per block 2|4|8; kb = 2 (batch <= 32): x staged in

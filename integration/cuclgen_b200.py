@@ -18,7 +18,7 @@ entry points through it).  Pure ctypes + numpy, like the reference: no torch.
 * The reference variants map onto the B200 kernels with their own knobs:
   ``conv_simple`` -> k_simple, ``conv_tiled`` -> k_tiled with the record's
   MNt / MNb / Kb / vw, ``conv_1x1`` / ``conv_fc`` -> the tcgen05 kernels.
-* ``conv_umma`` and ``conv_fc_stream`` (the B200-only variants the shipped
+* ``conv_umma``, ``conv_fc_stream`` and ``conv_wino`` (the B200-only variants the shipped
   TuneDBs name) are registered in ``cuclgen.variants.VARIANTS`` so that
   ``tuner.load_db`` (tuner.py:280 rejects unknown variant names) and
   ``select_variant`` (variants.py:840-856) accept the shipped B200 DBs.
@@ -42,7 +42,8 @@ from dataclasses import dataclass, fields
 _HERE = os.path.dirname(os.path.abspath(__file__))
 DEFAULT_LIB = os.path.join(os.path.dirname(_HERE), "paper_1611_06945_b200", "libb2conv.so")
 
-VAR_ID = {"conv_simple": 0, "conv_tiled": 1, "conv_1x1": 2, "conv_fc": 3, "conv_umma": 4, "conv_fc_stream": 5}
+VAR_ID = {"conv_simple": 0, "conv_tiled": 1, "conv_1x1": 2, "conv_fc": 3, "conv_umma": 4, "conv_fc_stream": 5,
+          "conv_wino": 6}
 B200_KEYS = ("BN", "sk", "sw", "dr", "tm", "oc", "cl", "pr")
 
 
@@ -223,8 +224,12 @@ def install(cuclgen, lib_path: str | None = None) -> Binding:
     class ConvFCStream(_B200Variant):
         name, rank = "conv_fc_stream", 0
 
+    class ConvWino(_B200Variant):
+        name, rank = "conv_wino", 0
+
     V.VARIANTS.setdefault("conv_umma", ConvUmma())
     V.VARIANTS.setdefault("conv_fc_stream", ConvFCStream())
+    V.VARIANTS.setdefault("conv_wino", ConvWino())
 
     orig_execute = R.execute_node
 

@@ -20,6 +20,7 @@
 #include "k_umma.cuh"
 #include "k_tma.cuh"
 #include "k_fcs.cuh"
+#include "k_wino.cuh"
 
 using namespace b2c;
 
@@ -158,6 +159,18 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             break;
         case B2C_VAR_UMMA:
             break;
+        case B2C_VAR_WINO: {  // Winograd F(2x2,3x3): transforms + 16 batched tcgen05 GEMMs (k_wino.cuh)
+            if (d->r != 3 || d->stride != 1 || d->pad > 1) { why = "conv_wino needs a 3x3, stride-1 conv with pad 0 or 1"; return B2C_INAPPLICABLE; }
+            if (d->prec != B2C_PREC_FP32) { why = "conv_wino: fp32-exact mode only"; return B2C_INAPPLICABLE; }
+            if (d->c % 4) { why = "conv_wino needs in_chans % 4 == 0 (16-byte TMA rows of V)"; return B2C_INAPPLICABLE; }
+            if (t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) { why = "conv_wino: tile_n in {64, 128, 192}"; return B2C_INAPPLICABLE; }
+            if (t->split_k < 0) { why = "split_k must be >= 0 (0 = stream-K)"; return B2C_BAD_ARGS; }
+            if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
+            if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
+            if (t->stages == 2 || t->cluster >= 2) { why = "conv_wino: single CTAs, 1 per SM"; return B2C_INAPPLICABLE; }
+            if (t->split_k > (d->c + 31) / 32) { why = "split_k exceeds the number of 32-wide K blocks"; return B2C_INAPPLICABLE; }
+            return B2C_OK;
+        }
         case B2C_VAR_FC_STREAM: {
             if (!(d->r == d->h && d->r == d->w && d->pad == 0 && d->oh == 1 && d->ow == 1)) {
                 why = "filters must cover the whole input with 1x1 output"; return B2C_INAPPLICABLE;
@@ -776,6 +789,166 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     return B2C_OK;
 }
 
+// ----------------------------------------------------------------------------- Winograd F(2x2,3x3)
+
+struct WinoPlan {
+    int tiles_y, tiles_x, P;   // 2x2 output tiles per image row / column, all tiles
+    b2c_conv_desc gd;          // the GEMM as a (P x C) * (OC x C)^T "fc" problem (act none)
+    int pix_rows, flt_rows, tiles_m, tiles_n, kblocks, kps, split, streamk, sk_grid, sk_maxc;
+    long long units;           // GEMM work units over all 16 z
+    size_t u_off, v_off, m_off, zb_off, part_off, sems_off, ws_bytes;
+};
+
+WinoPlan wino_plan(const b2c_conv_desc* d, const b2c_tune* t) {
+    WinoPlan p;
+    p.tiles_y = (d->oh + 1) / 2;
+    p.tiles_x = (d->ow + 1) / 2;
+    p.P = d->n * p.tiles_y * p.tiles_x;
+    // GEMM output M[z]: [P][OC] with swap_ab (its stores run along out channels), else [OC][P]
+    // (pixels on M: stores run along p) -- the geometry's PQ sets the stride (see epilogue_unit)
+    p.gd = t->swap_ab ? b2c_conv_desc{p.P, d->c, 1, 1, d->k, 1, 1, 0, 1, 1, 0, B2C_PREC_FP32}
+                      : b2c_conv_desc{1, d->c, 1, p.P, d->k, 1, 1, 0, 1, p.P, 0, B2C_PREC_FP32};
+    p.pix_rows = t->swap_ab ? t->tile_n : UMMA_M;
+    p.flt_rows = t->swap_ab ? UMMA_M : t->tile_n;
+    p.tiles_m = (p.P + p.pix_rows - 1) / p.pix_rows;
+    p.tiles_n = (d->k + p.flt_rows - 1) / p.flt_rows;
+    p.kblocks = (d->c + TM_BK - 1) / TM_BK;
+    const int want = std::max(1, std::min(t->split_k, p.kblocks));
+    p.kps = (p.kblocks + want - 1) / want;
+    p.split = (p.kblocks + p.kps - 1) / p.kps;
+    const long long tiles = 16ll * p.tiles_m * p.tiles_n;
+    p.streamk = t->split_k == 0 ? 1 : 0;
+    p.sk_grid = p.sk_maxc = 0;
+    size_t nslots = p.split > 1 ? (size_t)tiles * p.split : 0;
+    if (p.streamk) {
+        p.split = 1;
+        p.kps = p.kblocks;
+        const long long W = tiles * p.kblocks;
+        p.sk_grid = (int)std::min<long long>(W, num_sms());
+        const long long L = std::max<long long>(1, W / p.sk_grid);
+        p.sk_maxc = (int)((p.kblocks + L - 1) / L + 1);
+        nslots = (size_t)tiles * p.sk_maxc;
+    }
+    p.units = tiles * p.split;
+    const size_t f = sizeof(float);
+    p.u_off = 0;
+    p.v_off = align256(16ull * d->k * d->c * f);
+    p.m_off = p.v_off + align256(16ull * p.P * d->c * f);
+    p.zb_off = p.m_off + align256(16ull * p.P * d->k * f);
+    p.part_off = p.zb_off + align256((size_t)d->k * f);
+    p.sems_off = p.part_off + (nslots ? align256(nslots * t->tile_n * UMMA_M * f) : 0);
+    p.ws_bytes = p.sems_off + (nslots ? align256((size_t)tiles * sizeof(int)) : 256);
+    return p;
+}
+
+TconvEntry wino_pick(int bn, int swap) {
+    if (swap) {
+        switch (bn) {
+            case 64: return tconv_entry<64, true, 7, 1, 1>();
+            case 128: return tconv_entry<128, true, 7, 1, 1>();
+            case 192: return tconv_entry<192, true, 7, 1, 1>();
+        }
+    } else {
+        switch (bn) {
+            case 64: return tconv_entry<64, false, 7, 1, 1>();
+            case 128: return tconv_entry<128, false, 7, 1, 1>();
+            case 192: return tconv_entry<192, false, 7, 1, 1>();
+        }
+    }
+    return TconvEntry{nullptr, 0, 0};
+}
+
+int wino_filter_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+    const WinoPlan p = wino_plan(d, t);
+    if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+    const long long n = (long long)d->k * d->c;
+    k_wino_filter<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + p.u_off), d->k, d->c);
+    return B2C_OK;
+}
+
+int wino_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias, float* y,
+             void* ws, size_t ws_bytes, cudaStream_t st) {
+    const WinoPlan p = wino_plan(d, t);
+    if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+    int rc = load_tma_encoders();
+    if (rc) return rc;
+    TconvEntry e = wino_pick(t->tile_n, t->swap_ab);
+    if (!e.fn) return fail(B2C_INAPPLICABLE, "no Winograd GEMM kernel for this tile");
+    rc = ensure_smem_attr((const void*)e.fn, e.smem);
+    if (rc) return rc;
+    char* wsb = reinterpret_cast<char*>(ws);
+    float* u = reinterpret_cast<float*>(wsb + p.u_off);
+    float* v = reinterpret_cast<float*>(wsb + p.v_off);
+    float* m = reinterpret_cast<float*>(wsb + p.m_off);
+    if (!t->prepared) {
+        rc = wino_filter_impl(d, t, w, ws, ws_bytes, st);
+        if (rc) return rc;
+    }
+    // input transform: x -> V[16][P][C]
+    {
+        const int ws_cols = 2 * p.tiles_x + 2;
+        const size_t sm = (size_t)4 * ws_cols * 33 * sizeof(float);
+        rc = ensure_smem_attr((const void*)k_wino_input, (int)sm);
+        if (rc) return rc;
+        cudaError_t le = launch_pdl(k_wino_input, dim3(p.tiles_y, (d->c + WINO_CB - 1) / WINO_CB, d->n), dim3(256), sm, st, 1,
+                                    x, v, (int)d->c, (int)d->h, (int)d->w, (int)d->pad, p.tiles_y, p.tiles_x, (long long)p.P);
+        if (le != cudaSuccess) return cuda_fail(le, "k_wino_input launch");
+    }
+    // 16 GEMMs M[z] = V[z] U[z]^T on the tcgen05 3xTF32 kernel (MODE 7)
+    {
+        CUtensorMap tm_v, tm_u;
+        const cuuint64_t vd[3] = {(cuuint64_t)d->c, (cuuint64_t)p.P, 16};
+        const cuuint64_t vs[2] = {(cuuint64_t)d->c * 4, (cuuint64_t)p.P * d->c * 4};
+        const cuuint32_t vb[3] = {(cuuint32_t)TM_BK, (cuuint32_t)p.pix_rows, 1};
+        const cuuint64_t ud[3] = {(cuuint64_t)d->c, (cuuint64_t)d->k, 16};
+        const cuuint64_t us[2] = {(cuuint64_t)d->c * 4, (cuuint64_t)d->k * d->c * 4};
+        const cuuint32_t ub[3] = {(cuuint32_t)TM_BK, (cuuint32_t)p.flt_rows, 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = g_enc_tiled(&tm_v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, v, vd, vs, vb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeTiled (Winograd V) failed (" + std::to_string((int)r) + ")");
+        r = g_enc_tiled(&tm_u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, u, ud, us, ub, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeTiled (Winograd U) failed (" + std::to_string((int)r) + ")");
+        TArgs a = {};
+        a.g = make_geom(&p.gd);
+        a.wpk = u;
+        a.bias = reinterpret_cast<const float*>(wsb + p.zb_off);  // unused by MODE 7 (no bias in the GEMM)
+        a.y = m;
+        a.split = p.split;
+        a.kps = p.kps;
+        a.kblocks = p.kblocks;
+        a.streamk = p.streamk;
+        a.sk_maxc = p.sk_maxc;
+        a.tiles_n = p.tiles_n;
+        a.tiles_m = p.tiles_m;
+        a.units = (int)p.units;
+        a.fCB = FastDiv(1u);
+        a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
+        a.ws = reinterpret_cast<float*>(wsb + p.part_off);
+        a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
+        a.trace = g_trace_on & 15;
+        a.kb_period = p.kblocks;
+        a.ksteps_last = std::min(TM_BK / 8, std::max(1, (d->c - TM_BK * (p.kblocks - 1) + 7) / 8));
+        const int grid = p.streamk ? p.sk_grid : (int)std::min<long long>(p.units, num_sms());
+        cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, 1, tm_v, tm_u, a);
+        if (le != cudaSuccess) return cuda_fail(le, "Winograd GEMM launch");
+    }
+    // output transform: M -> y (+ bias, ReLU)
+    {
+        const size_t sm = (size_t)WINO_CB * 2 * (2 * p.tiles_x + 1) * sizeof(float);
+        auto kout = t->swap_ab ? k_wino_output<false> : k_wino_output<true>;
+        rc = ensure_smem_attr((const void*)kout, (int)sm);
+        if (rc) return rc;
+        cudaError_t le = launch_pdl(kout, dim3(p.tiles_y, (d->k + WINO_CB - 1) / WINO_CB, d->n), dim3(256), sm, st, 1,
+                                    (const float*)m, bias, y, (int)d->k, (int)d->oh, (int)d->ow, p.tiles_y, p.tiles_x,
+                                    (long long)p.P, (int)d->act);
+        if (le != cudaSuccess) return cuda_fail(le, "k_wino_output launch");
+    }
+    return B2C_OK;
+}
+
 int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const float* w, const float* bias,
              float* y, void* ws, size_t ws_bytes, cudaStream_t st) {
     std::string why;
@@ -801,6 +974,10 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
             fn<<<grid, t->mnb0 * t->mnb1, sm, st>>>(g, x, w, bias, y, t->mnb0, t->mnb1, t->kb);
             break;
         }
+        case B2C_VAR_WINO:
+            rc = wino_fwd(d, t, x, w, bias, y, ws, ws_bytes, st);
+            if (rc) return rc;
+            break;
         case B2C_VAR_FC_STREAM: {
             using FcsKernel = void (*)(const float*, const float*, const float*, float*, int, int, int, int);
             if (t->kb == 2) {
@@ -943,6 +1120,7 @@ int b2c_conv_applies(const b2c_conv_desc* d, const b2c_tune* t, char* reason, si
 size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t) {
     std::string why;
     if (applies_impl(d, t, why)) return 0;
+    if (t->variant == B2C_VAR_WINO) return wino_plan(d, t).ws_bytes;
     if (!is_umma(t->variant)) return 0;
     return umma_plan(d, t).ws_bytes;
 }
@@ -952,9 +1130,11 @@ int b2c_conv_prepare(const b2c_conv_desc* d, const b2c_tune* t, const float* w, 
     std::string why;
     int rc = applies_impl(d, t, why);
     if (rc) return fail(rc, why);
-    if (!is_umma(t->variant)) return B2C_OK;
+    if (!is_umma(t->variant) && t->variant != B2C_VAR_WINO) return B2C_OK;
     if (!w) return fail(B2C_BAD_ARGS, "null filter pointer");
-    rc = pack_impl(d, t, w, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+    rc = t->variant == B2C_VAR_WINO
+             ? wino_filter_impl(d, t, w, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream))
+             : pack_impl(d, t, w, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
     if (rc) return rc;
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return cuda_fail(le, "pack launch");
@@ -1037,6 +1217,10 @@ int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx
     // The split-K / stream-K tickets and the grid-barrier counter must be zero at
     // rest; the scratch may be fresh (uninitialised) device memory, so zero them
     // on the stream (a few bytes; the partials themselves need no init).
+    if (wsb && t->variant == B2C_VAR_WINO) {
+        const WinoPlan wp = wino_plan(d, t);
+        B2C_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ws) + wp.sems_off, 0, wp.ws_bytes - wp.sems_off, st));
+    }
     if (wsb && is_umma(t->variant)) {
         const UmmaPlan up = umma_plan(d, t);
         if (up.nhwc_off > up.sems_off)
@@ -1069,6 +1253,7 @@ int64_t b2c_conv_bytes(const b2c_conv_desc* d) {
 int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
     (void)d;
     if (!t) return 0;
+    if (t->variant == B2C_VAR_WINO) return 3 + (t->prepared ? 0 : 1);  // input transform, GEMM, output transform
     const int pack = (is_umma(t->variant) && !t->prepared && !(t->tma && t->variant == B2C_VAR_FC)) ? 1 : 0;
     const bool sep = std::getenv("B2C_FUSED_NHWC") == nullptr || (t->tma == 2 && d && d->c <= 4);
     const int nhwc = (is_umma(t->variant) && t->tma && t->tma != 3 && t->tma != 4 && t->variant != B2C_VAR_FC && sep) ? 1 : 0;
@@ -1087,6 +1272,10 @@ int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t) {
         case B2C_VAR_TILED: {
             const int BM = t->mnb0 * t->mnt0, BN = t->mnb1 * t->mnt1;
             return ((g.M + BM - 1) / BM) * ((g.OC + BN - 1) / BN);
+        }
+        case B2C_VAR_WINO: {
+            const WinoPlan p = wino_plan(d, t);
+            return p.streamk ? p.sk_grid : (int)std::min<long long>(p.units, num_sms());
         }
         case B2C_VAR_FC_STREAM:
             return t->kb == 2 ? (g.OC + t->mnb0 * t->mnt1 - 1) / (t->mnb0 * t->mnt1) : (g.OC + t->mnt1 - 1) / t->mnt1;

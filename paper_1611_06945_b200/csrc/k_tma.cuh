@@ -29,6 +29,9 @@
 //     pixels x 32 window floats per box into the SWIZZLE_128B layout: 128-byte
 //     rows instead of MODE 3's 16-byte ones (the TMA unit issues ~0.75 rows
 //     per clock per SM, so row width sets its throughput).
+//   * MODE 7 (Winograd F(2x2,3x3), conv_wino): 16 independent GEMMs
+//     M[z] = V[z] * U[z]^T over the transformed tiles (k_wino.cuh): MODE 1 with a
+//     third TMA coordinate z, no bias / activation (the output transform adds them).
 //   * MODE 1 (fc, variants.py:328-373): the whole-image filter makes both
 //     operands plain row-major [rows][K] matrices (x as [img][ic*h*w], w as
 //     [oc][ic*h*w]), loaded raw by 2-D tiled TMA: the fc6 weights (151 MB)
@@ -82,9 +85,10 @@ constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 // filter tile (B rows) and its own 128 accumulator rows.
 template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
-    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && CL == 1), "bf16: pixels on M, packed filters");
+    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && MODE != 7 && CL == 1), "bf16: pixels on M, packed filters");
+    static constexpr bool RAW_B = MODE == 1 || MODE == 7;  // both operands raw [rows][K] matrices by TMA (no pack)
     static_assert((MODE != 5 && MODE != 6) || CL != 2, "MODE 5/6: no multicast pairs");
-    static_assert(CL == 1 || ((CL == 2 || CL == 3) && !SWAP && MODE != 1 && OCC == 1), "pairs share B = packed filters");
+    static_assert(CL == 1 || ((CL == 2 || CL == 3) && !SWAP && !RAW_B && OCC == 1), "pairs share B = packed filters");
     static constexpr bool PAIR = CL == 3;  // 2-SM UMMA
     static_assert(!PAIR || (BN >= 64 && BN <= 192), "2-SM UMMA: N = BN in [64, 192] (two accumulators + A slots in TMEM)");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
@@ -102,7 +106,7 @@ struct TmaCfg {
     // it there as raw + lo from the smem image the TMA (or bulk copy) wrote.
     // lo is computed on the way (filters, when they are A, are packed raw-only).
     static constexpr bool A_PRESPLIT = false;
-    static constexpr bool B_SPLIT = SWAP || MODE == 1;  // B raw from TMA: lo computed into smem
+    static constexpr bool B_SPLIT = SWAP || RAW_B;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
     static constexpr int B_BYTES = PREC ? BN * 64 : (PAIR ? 1 : 2) * BN * 128;  // bf16 | raw + lo (a pair: half the rows each)
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
@@ -125,7 +129,7 @@ struct TmaCfg {
     static constexpr int A_SLOTS = A_SLOTS_FIT < 4 ? A_SLOTS_FIT : 4;
     static_assert(ACC_COLS + A_SLOTS * 64 <= TMEM_COLS, "TMEM budget");
     static constexpr bool SW128 = MODE != 3;
-    static constexpr uint32_t BYTES = PIX_ROWS * 128 + (MODE == 1 ? FLT_ROWS * 128 : FLT_CTA);
+    static constexpr uint32_t BYTES = PIX_ROWS * 128 + (RAW_B ? FLT_ROWS * 128 : FLT_CTA);
     // barrier arrival counts (a pair's leader counts its peer's split / drain warps too)
     static constexpr int SPLIT_ARRIVALS = PAIR ? 2 * (TM_SPLIT_THREADS / 32) : TM_SPLIT_THREADS;
     static constexpr int DRAIN_ARRIVALS = PAIR ? 2 * (DRAIN_THREADS / 32) : DRAIN_THREADS;
@@ -209,10 +213,13 @@ __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     Unit w;
     w.z = u % a.split;
     const int t2 = u / a.split;
-    const int nt = t2 % a.tiles_n;
-    const int mt = CL >= 2 ? 2 * (t2 / a.tiles_n) + rank : t2 / a.tiles_n;
+    // MODE 7: tile t2 of the batched GEMM = (z, pixel tile, filter tile), z outermost
+    const int zb = MODE == 7 ? t2 / (a.tiles_m * a.tiles_n) : 0;
+    const int t3 = MODE == 7 ? t2 - zb * (a.tiles_m * a.tiles_n) : t2;
+    const int nt = t3 % a.tiles_n;
+    const int mt = CL >= 2 ? 2 * (t3 / a.tiles_n) + rank : t3 / a.tiles_n;
     w.ghost = mt >= a.tiles_m;
-    w.t = mt * a.tiles_n + nt;
+    w.t = MODE == 7 ? t2 : mt * a.tiles_n + nt;
     w.m0 = mt * PIX_ROWS;
     w.n0 = nt * FLT_ROWS;
     w.kb_begin = w.z * a.kps;
@@ -224,7 +231,8 @@ __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
         w.oy0 = (r / a.tiles_x) * a.by;
         w.ox0 = (r % a.tiles_x) * a.bx;
     } else {
-        w.b = w.oy0 = w.ox0 = 0;
+        w.b = zb;  // MODE 7: the GEMM's z (0 otherwise)
+        w.oy0 = w.ox0 = 0;
     }
     w.nsplit = a.split;
     w.pslot0 = w.t * a.split;
@@ -572,7 +580,7 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
             for (int j = 0; j < DC; ++j) acc[j] += __ldcg(base + ((size_t)zz * BN + c_begin + j) * TM_M + row);
         }
     }
-    float* __restrict__ yp = a.y;
+    float* __restrict__ yp = a.y + (MODE == 7 ? (long long)w.b * g.M * g.OC : 0ll);  // MODE 7: M[z]
     if (!SWAP) {  // row = output pixel, columns = out_chans
         long long row_out;
         if (MODE == 5) {  // run of 128 pixels of image b starting at ox0
@@ -616,7 +624,7 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
     } else {  // row = out_chan, columns = output pixels
         const int oc = w.n0 + row;
         if (oc >= g.OC) return;
-        const float rb = __ldg(a.bias + oc);
+        const float rb = MODE == 7 ? 0.0f : __ldg(a.bias + oc);
         const int act = g.act;
 #pragma unroll
         for (int j = 0; j < DC; ++j) acc[j] = apply_act(acc[j] + rb, act);
@@ -688,7 +696,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     }
     if (warp == Cfg::LOAD_WARP && lane == 0) {
         tma_prefetch_desc(&tm_pix);
-        if (MODE == 1) tma_prefetch_desc(&tm_flt);
+        if (MODE == 1 || MODE == 7) tma_prefetch_desc(&tm_flt);
     }
     tc_fence_before();
     __syncthreads();
@@ -700,7 +708,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     // The loader may stream the first stages' packed filters (constant, written
     // by an earlier synchronised b2c_conv_prepare) while the previous kernel
     // (the x re-layout) is still running; everything else waits for it here.
-    const bool early = a.flt_early && MODE != 1 && !a.relayout && warp == Cfg::LOAD_WARP;
+    const bool early = a.flt_early && !Cfg::RAW_B && !a.relayout && warp == Cfg::LOAD_WARP;
     if (!early) pdl_wait();
     if (a.relayout) fused_relayout(a, smem + TM_HDR + 1024);
     if (tid == 0) B2C_TRACE(a.trace, 3);
@@ -771,7 +779,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
 #pragma unroll
             for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
             float bpre = 0.0f;  // this thread's share of the unit's biases, loaded under the main loop
-            if (!SWAP && dtid < BN && w.n0 + dtid < g.OC) bpre = __ldg(a.bias + w.n0 + dtid);
+            if (!SWAP && MODE != 7 && dtid < BN && w.n0 + dtid < g.OC) bpre = __ldg(a.bias + w.n0 + dtid);
             const int nch = (w.nkb + G - 1) / G;
             for (int c = 0; c < nch; ++c, ++cidx) {
                 const int slot = cidx & 1;
@@ -946,6 +954,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 if (MODE == 1) {
                     tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
                     tma_load_2d(sbase + Cfg::FLT_OFF, &tm_flt, bar, kb * TM_BK, w.n0);
+                } else if (MODE == 7) {  // V[z] rows and U[z] rows: (k, row, z)
+                    tma_load_3d(pix, &tm_pix, bar, kb * TM_BK, w.m0, w.b);
+                    tma_load_3d(sbase + Cfg::FLT_OFF, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
                 } else {
                     if (MODE == 2) {
                         tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);

@@ -302,6 +302,27 @@ class ConvFC(_UmmaFamily):
     name, rank, vid = "conv_fc", 4, backend.VAR_FC
 
 
+class ConvWino(Variant):
+    """Winograd F(2x2,3x3) (the paper's gap to cuDNN on
+    3x3): for 3x3, stride-1, pad <= 1 convs, 16 batched tcgen05
+    3xTF32 GEMMs between the transformed input tiles V = B^T d B and the
+    transformed filters U = G g G^T (built once by b2c_conv_prepare), then
+    y = A^T M A + bias, ReLU.  2.25x fewer multiplies than direct conv; the
+    transforms are exact-coefficient fp32 adds, so the fp32 reference tolerance
+    applies unchanged.  Knobs: bn (GEMM N tile 64|128|192), split_k (0 =
+    stream-K), swap_ab."""
+
+    name, rank, vid = "conv_wino", 1, backend.VAR_WINO
+
+    def default_params(self, node, edges):
+        return TuneParams(bn=128, split_k=1, tma=1)
+
+    def space(self, node, edges):
+        out = [TuneParams(bn=bn, split_k=sk, swap_ab=sw, tma=1) for sw in (False, True) for bn in (64, 128, 192)
+               for sk in (1, 2, 4, 0)]
+        return [p for p in out if self.applies(node, edges, p) is None]
+
+
 class ConvFCStream(Variant):
     """ConvFC (variants.py:328-373) as an fp32 FFMA weight-streaming kernel for
     small batch, where the op is HBM-bound.  Kb=1 (batch <= 8): warps split K,
@@ -391,7 +412,7 @@ class Xpose(_NodeVariant):
 
 
 VARIANTS: dict = {v.name: v for v in (ConvSimple(), ConvTiled(), ConvUmma(), Conv1x1(), ConvFC(), ConvFCStream(),
-                                      PoolMax(), Activation(), Xpose())}
+                                      ConvWino(), PoolMax(), Activation(), Xpose())}
 
 
 def variants_for_kind(kind: str) -> list:

@@ -69,6 +69,9 @@ def _variant_params(g):
                     TuneParams(bn=128, tma=3, cl=3), TuneParams(bn=128, split_k=0, tma=1, cl=3),
                     TuneParams(bn=64, split_k=0, tma=4, cl=3)):
             out.append((v, prm))
+    out += [("conv_wino", p) for p in (TuneParams(bn=64, tma=1), TuneParams(bn=128, split_k=2, tma=1),
+                                       TuneParams(bn=192, split_k=0, tma=1), TuneParams(bn=64, swap_ab=True, tma=1),
+                                       TuneParams(bn=128, swap_ab=True, split_k=0, tma=1))]
     out += [("conv_fc_stream", TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)),
             ("conv_fc_stream", TuneParams(mnt=(1, 2), mnb=(4, 1), kb=1, vw=1)),
             ("conv_fc_stream", TuneParams(mnt=(1, 8), mnb=(2, 1), kb=1, vw=1)),

@@ -108,7 +108,7 @@ def test_tune_params_string_roundtrip_and_reference_form():
 
 def test_variant_rank_order_and_heuristic():
     assert [v.name for v in variants_for_kind("Convolution")] == ["conv_fc_stream", "conv_fc", "conv_1x1", "conv_umma",
-                                                                  "conv_tiled", "conv_simple"]
+                                                                  "conv_tiled", "conv_wino", "conv_simple"]
     g = g_of(6, 1, 0, 16, (2, 8, 6, 6))
     assert select_variant(g.node("conv"), g.edges)[0].name == "conv_fc_stream"  # batch <= 8: weight streaming
     g = g_of(6, 1, 0, 16, (20, 8, 6, 6))

@@ -37,9 +37,12 @@ for spec in a.ops.split(","):
     torch.cuda.synchronize()
     terms = op.in_chans * op.ksz * op.ksz
     for ptxt in a.params:
+        vname = None
+        if ":" in ptxt.split(",")[0]:  # "conv_wino:BN=128,..." names the variant
+            vname, ptxt = ptxt.split(":", 1)
         p = TuneParams.from_string(BASE + ptxt)
-        vname = "conv_fc" if (op.ksz == op.in_y and op.pad == 0 and "fc" in ptxt) else (
-            "conv_1x1" if op.ksz == 1 else "conv_umma")
+        vname = vname or ("conv_fc" if (op.ksz == op.in_y and op.pad == 0 and "fc" in ptxt) else (
+            "conv_1x1" if op.ksz == 1 else "conv_umma"))
         v = VARIANTS[vname]
         why = v.applies(node, g.edges, p)
         if why:
