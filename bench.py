@@ -73,9 +73,9 @@ def parse_args(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--batches", default="1,5,20")
-    ap.add_argument("--prec", choices=("fp32", "bf16"), default="fp32",
+    ap.add_argument("--prec", choices=("fp32", "bf16", "fp8"), default="fp32",
                     help="fp32: fp32-exact (3xTF32 / FFMA, the headline); bf16: bf16 operands, fp32 accumulate "
-                         "(separately stated tolerance rel 4e-3)")
+                         "(separately stated tolerance rel 4e-3); fp8: e4m3 operands, fp32 accumulate (rel 0.13, the per-product rounding bound)")
     ap.add_argument("--db", default=None,
                     help="latency TuneDB for the per-op runtimes (default: shipped B200 DB of the precision)")
     ap.add_argument("--sweep-db", default=None,
@@ -476,7 +476,7 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     if args.debug_flags:
         be.lib().b2c_debug_trace_enable(args.debug_flags & ~1)  # never the (CTA-0 trace) bit
     batches = [int(b) for b in args.batches.split(",")]
-    prec = 1 if args.prec == "bf16" else 0
+    prec = {"fp32": 0, "bf16": 1, "fp8": 2}[args.prec]
     db_path = args.db or tuner.shipped_db_path(args.prec)
     db = tuner.load_db(db_path) if (os.path.exists(db_path) and not args.heuristic) else None
     sdb_path = args.sweep_db or tuner.shipped_db_path(args.prec + "_sweep")
@@ -673,7 +673,8 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
         return
     peaks = load_peaks()
     tf32_mode = tf32 / 3.0  # 3xTF32: three TF32 MMA passes per useful product
-    mode_peak = peaks["bf16_tflops"] if prec else tf32_mode
+    # fp8: the nominal dense fp8 rate is 2x bf16 (no measured fp8 peak in MEASURED_PEAKS.json)
+    mode_peak = {0: tf32_mode, 1: peaks["bf16_tflops"], 2: 2.0 * peaks["bf16_tflops"]}[prec]
 
     def frac_of_roof(fl_i, by_i, ms):
         t_roof = max(fl_i / (mode_peak * 1e12), by_i / (peaks["hbm_gbs"] * 1e9))
@@ -691,7 +692,8 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
             roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": peaks["bf16_tflops"],
                     "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
                     "mode_peak": round(mode_peak, 1), "frac_of_mode_peak": round(achieved / mode_peak, 4),
-                    "mode_peak_note": ("bf16 mode: measured bf16 dense peak" if prec else
+                    "mode_peak_note": ("bf16 mode: measured bf16 dense peak" if prec == 1 else
+                                       "fp8 mode: 2 x the measured bf16 dense peak (nominal fp8 rate)" if prec == 2 else
                                        "fp32-exact 3xTF32 ceiling = TF32 dense measured in this run "
                                        "(cuBLAS 8192^3) / 3 passes")}
         else:
@@ -758,7 +760,8 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "strong" if shard_mode else "weak",
         "vs_baseline": None, "dtype": args.prec, "data": "synthetic",
-        "config": {"workload": WORKLOAD if not prec else WORKLOAD.replace(", fp32", ", bf16 operands / fp32 accumulate"),
+        "config": {"workload": WORKLOAD if not prec else WORKLOAD.replace(
+                       ", fp32", ", bf16 operands / fp32 accumulate" if prec == 1 else ", e4m3 operands / fp32 accumulate"),
                    "global_batch": ",".join(str(b if shard_mode else b * world) for b in batches),
                    "sharding": ("per-unit image slabs over ranks (20 over 8: 3,3,3,3,2,2,2,2; smaller batches "
                                 "by single images, LPT) - strong" if shard_mode

@@ -73,6 +73,8 @@ extern "C" {
 /* Precision modes. */
 #define B2C_PREC_FP32 0 /* fp32-exact: FFMA, or 3xTF32 split on the tensor cores */
 #define B2C_PREC_BF16 1 /* bf16 operands, fp32 accumulate (separately stated tolerance) */
+#define B2C_PREC_FP8 2  /* e4m3 operands (round to nearest, saturating at +-448, no scaling), fp32
+                           accumulate: tcgen05 kind::f8f6f4 (separately stated tolerance) */
 
 /* One convolution, the C form of (ConvParams, input DimsSpec, fused_activation):
  * ConvParams(ksz, stride, pad, out_chans) frontend.py:56-65; output extent
@@ -84,7 +86,7 @@ typedef struct b2c_conv_desc {
     int32_t stride, pad;
     int32_t oh, ow; /* must equal (h + 2*pad - r)/stride + 1 (and same for w) */
     int32_t act;    /* 0 none, 1 relu ("(ov > 0) ? ov : 0", variants.py:164) */
-    int32_t prec;   /* B2C_PREC_* */
+    int32_t prec;   /* B2C_PREC_*: 0 fp32-exact, 1 bf16, 2 fp8 (e4m3) */
 } b2c_conv_desc;
 
 /* Variant + tuning knobs, the C form of TuneParams (variants.py:39-91).
@@ -119,6 +121,9 @@ typedef struct b2c_tune {
                         M = 256 issued by the leader CTA, each CTA holding half of the filter tile's rows
                         (half the filter L2 and shared-memory traffic per CTA; tile_n 64 | 128 | 192,
                         fp32-exact mode, tma 1 | 3 | 4);
+                        4 = split-K clusters: the split_k (2..8) CTAs of an output tile form one thread-block
+                        cluster and the leader sums the partials over distributed shared memory (no global
+                        partials / tickets; tile_n 32 | 64 conv tiles with tma 1 | 3 | 4, or the fc swap tile);
                         0/1 = single CTAs.  Pairs need swap_ab = 0 and a conv (not fc) variant. */
 } b2c_tune;
 

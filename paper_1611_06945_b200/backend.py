@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 B2C_OK, B2C_INAPPLICABLE, B2C_BAD_ARGS, B2C_CUDA_ERROR, B2C_UNSUPPORTED = range(5)
 VAR_SIMPLE, VAR_TILED, VAR_1X1, VAR_FC, VAR_UMMA, VAR_FC_STREAM, VAR_WINO = range(7)
-PREC_FP32, PREC_BF16 = 0, 1
+PREC_FP32, PREC_BF16, PREC_FP8 = 0, 1, 2
 
 # Every symbol include/b2conv.h declares (checked by tests/test_abi.py).
 EXPORTS = (

@@ -61,7 +61,8 @@ int check_desc(const b2c_conv_desc* d) {
     const long long wk = (long long)d->k * d->c * d->r * d->r;
     if (xin >= (1ll << 31) || yout >= (1ll << 31) || wk >= (1ll << 31))
         return fail(B2C_UNSUPPORTED, "tensor exceeds 2^31 elements");
-    if (d->prec != B2C_PREC_FP32 && d->prec != B2C_PREC_BF16) return fail(B2C_BAD_ARGS, "prec must be 0 (fp32) or 1 (bf16)");
+    if (d->prec != B2C_PREC_FP32 && d->prec != B2C_PREC_BF16 && d->prec != B2C_PREC_FP8)
+        return fail(B2C_BAD_ARGS, "prec must be 0 (fp32), 1 (bf16) or 2 (fp8 e4m3)");
     return B2C_OK;
 }
 
@@ -128,6 +129,18 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             why = "bf16 mode: tile_n in {32, 64, 128, 192}"; return B2C_INAPPLICABLE;
         }
     }
+    if (d->prec == B2C_PREC_FP8) {
+        // e4m3 operands / fp32 accumulate: the TMA tcgen05 kernel with pixels on M
+        if (t->variant != B2C_VAR_UMMA && t->variant != B2C_VAR_1X1) {
+            why = "fp8 mode: tcgen05 conv_umma / conv_1x1 only"; return B2C_INAPPLICABLE;
+        }
+        if (!t->tma || t->tma == 2 || t->swap_ab || t->cluster >= 2 || t->stages == 2) {
+            why = "fp8 mode: TMA kernel (tma=1|3|4), swap_ab=0, single CTAs"; return B2C_INAPPLICABLE;
+        }
+        if (t->tile_n != 32 && t->tile_n != 64 && t->tile_n != 128) {
+            why = "fp8 mode: tile_n in {32, 64, 128}"; return B2C_INAPPLICABLE;
+        }
+    }
     switch (t->variant) {
         case B2C_VAR_SIMPLE:
             return B2C_OK;
@@ -190,7 +203,20 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     // tcgen05 family
     if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192"; return B2C_INAPPLICABLE; }
     if (t->split_k < 0 || (t->split_k == 0 && !t->tma)) { why = "split_k must be >= 1 (0 = stream-K, TMA kernel only)"; return B2C_BAD_ARGS; }
-    if (t->cluster < 0 || t->cluster > 3) { why = "cluster must be 0..3"; return B2C_BAD_ARGS; }
+    if (t->cluster < 0 || t->cluster > 4) { why = "cluster must be 0..4"; return B2C_BAD_ARGS; }
+    if (t->cluster == 4) {  // split-K over a thread-block cluster, fixup through DSMEM
+        if (!t->tma || t->split_k < 2 || t->split_k > 8 || t->stages == 2 || d->prec != B2C_PREC_FP32) {
+            why = "cluster split-K (cluster=4): TMA kernel, split_k 2..8, 1 CTA/SM, fp32-exact mode";
+            return B2C_INAPPLICABLE;
+        }
+        const bool fc_swap = t->variant == B2C_VAR_FC && t->swap_ab && t->tile_n == 32;
+        const bool conv = t->variant != B2C_VAR_FC && !t->swap_ab && (t->tile_n == 32 || t->tile_n == 64) &&
+                          (t->tma == 1 || t->tma == 3 || t->tma == 4) && !(t->tma == 1 && d->c <= 4);
+        if (!fc_swap && !conv) {
+            why = "cluster split-K: tile_n 32|64 conv tiles (tma 1|3|4, pixels on M) or the fc swap tile (tile_n 32)";
+            return B2C_INAPPLICABLE;
+        }
+    }
     if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K: single CTAs or 2-SM pairs"; return B2C_INAPPLICABLE; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
@@ -308,12 +334,13 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.kps = (p.kblocks + want - 1) / want;
     p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
     // packed filters: raw | lo per K block; raw only when the TMA kernel takes them as its TMEM A operand
-    p.parts = (p.tma && t->swap_ab) || d->prec == B2C_PREC_BF16 ? 1 : 2;
-    const size_t row_bytes = d->prec == B2C_PREC_BF16 ? UMMA_BK * 2 : UMMA_BK * sizeof(float);  // per K block
+    p.parts = (p.tma && t->swap_ab) || d->prec != B2C_PREC_FP32 ? 1 : 2;
+    const size_t row_bytes = d->prec == B2C_PREC_BF16 ? UMMA_BK * 2 : d->prec == B2C_PREC_FP8 ? UMMA_BK
+                                                                                           : UMMA_BK * sizeof(float);  // per K block
     p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * p.parts * p.flt_rows * row_bytes;
     p.streamk = (t->tma && t->split_k == 0) ? 1 : 0;
     p.sk_grid = p.sk_maxc = 0;
-    size_t nslots = p.split > 1 ? (size_t)p.tiles * p.split : 0;
+    size_t nslots = (p.split > 1 && t->cluster != 4) ? (size_t)p.tiles * p.split : 0;  // cluster split-K: DSMEM
     if (p.streamk) {
         // 2-SM pairs share units (two neighbouring pixel tiles): stream-K over pair-units, one share per pair
         const bool pair = t->cluster == 3;
@@ -380,6 +407,13 @@ int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* w
     if (p.wpk_bytes == 0) return B2C_OK;  // TMA fc path reads raw filters
     if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
     const Geom g = make_geom(d);
+    if (d->prec == B2C_PREC_FP8) {
+        const long long total = (long long)p.wpk_bytes;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+        k_pack_filters_e4m3<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<uint8_t*>(ws), p.flt_rows, p.kblocks,
+                                                    FastDiv((uint32_t)p.cblocks), p.kmode, total);
+        return B2C_OK;
+    }
     if (d->prec == B2C_PREC_BF16) {
         const long long total = (long long)p.wpk_bytes / 2;
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
@@ -555,6 +589,15 @@ cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem,
     return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
 }
 
+// Multiply-shift divisors for the kernel's unit decomposition (unit_of, k_tma.cuh).
+void set_unit_divs(TArgs& a) {
+    a.fSplit = FastDiv((uint32_t)std::max(1, a.split));
+    a.fTilesN = FastDiv((uint32_t)std::max(1, a.tiles_n));
+    a.fTilesMN = FastDiv((uint32_t)std::max(1, a.tiles_m * a.tiles_n));
+    a.fPerImg = FastDiv((uint32_t)std::max(1, a.tiles_x * a.tiles_y));
+    a.fTilesX = FastDiv((uint32_t)std::max(1, a.tiles_x));
+}
+
 using TconvKernel = void (*)(const CUtensorMap, const CUtensorMap, TArgs);
 
 struct TconvEntry {
@@ -580,6 +623,16 @@ TconvEntry tconv_pick_bf16(int bn) {
     return TconvEntry{nullptr, 0, 0};
 }
 
+template <int MODE>
+TconvEntry tconv_pick_fp8(int bn) {
+    switch (bn) {
+        case 32: return tconv_entry<32, false, MODE, 1, 1, 2>();
+        case 64: return tconv_entry<64, false, MODE, 1, 1, 2>();
+        case 128: return tconv_entry<128, false, MODE, 1, 1, 2>();
+    }
+    return TconvEntry{nullptr, 0, 0};
+}
+
 template <bool SWAP, int MODE>
 TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
     if (cl == 2) {
@@ -590,6 +643,18 @@ TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
                 case 128: return tconv_entry<128, false, MODE, 1, 2>();
                 case 192: return tconv_entry<192, false, MODE, 1, 2>();
             }
+        }
+        return TconvEntry{nullptr, 0, 0};
+    }
+    if (cl == 4) {  // split-K clusters (DSMEM fixup)
+        if constexpr (!SWAP && (MODE == 0 || MODE == 5 || MODE == 6)) {
+            switch (bn) {
+                case 32: return tconv_entry<32, false, MODE, 1, 4>();
+                case 64: return tconv_entry<64, false, MODE, 1, 4>();
+            }
+        }
+        if constexpr (SWAP && MODE == 1) {
+            if (bn == 32) return tconv_entry<32, true, 1, 1, 4>();
         }
         return TconvEntry{nullptr, 0, 0};
     }
@@ -656,12 +721,16 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
     const int mode = t->tma == 4 ? 6 : t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
-    const int cl = (t->cluster == 2 || t->cluster == 3) ? t->cluster : 1;
+    const int cl = (t->cluster >= 2 && t->cluster <= 4) ? t->cluster : 1;
     TconvEntry e{nullptr, 0, 0};
     if (d->prec == B2C_PREC_BF16)
         e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
             : mode == 4 ? tconv_pick_bf16<4>(t->tile_n) : mode == 5 ? tconv_pick_bf16<5>(t->tile_n)
             : mode == 6 ? tconv_pick_bf16<6>(t->tile_n)
+            : TconvEntry{nullptr, 0, 0};
+    else if (d->prec == B2C_PREC_FP8)
+        e = mode == 0 ? tconv_pick_fp8<0>(t->tile_n) : mode == 4 ? tconv_pick_fp8<4>(t->tile_n)
+            : mode == 5 ? tconv_pick_fp8<5>(t->tile_n) : mode == 6 ? tconv_pick_fp8<6>(t->tile_n)
             : TconvEntry{nullptr, 0, 0};
     else
         e = tconv_pick(t->tile_n, t->swap_ab, mode, occ, cl);
@@ -746,13 +815,14 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.tiles_n = p.grid_y;
     a.tiles_m = p.grid_x;
     // CL = 2: units are pair-units (two neighbouring pixel tiles)
-    a.units = (cl >= 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
+    a.units = ((cl == 2 || cl == 3) ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
     a.bx = p.bx;
     a.by = p.by;
     a.tiles_x = p.tiles_x;
     a.tiles_y = p.tiles_y;
     a.box_w = p.box_w;
     a.fCB = FastDiv((uint32_t)p.cblocks);
+    set_unit_divs(a);
     a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
     a.ws = reinterpret_cast<float*>(wsb + p.part_off);
     a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
@@ -782,9 +852,11 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         if (no_skip) a.ksteps_last = TM_BK / 8;
     }
     const int grid = p.streamk ? p.sk_grid
+                     : cl == 4  ? p.split * std::min(p.tiles, std::max(1, num_sms() / p.split))  // whole clusters
                      : cl >= 2  ? 2 * std::min(a.units, num_sms() / 2)
                                 : std::min(a.units, occ * num_sms());
-    cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, cl >= 2 ? 2 : 1, tm_pix, tm_flt, a);
+    const int cdim = cl == 4 ? p.split : cl >= 2 ? 2 : 1;
+    cudaError_t le = launch_pdl(e.fn, dim3(grid), dim3(e.threads), (size_t)e.smem, st, cdim, tm_pix, tm_flt, a);
     if (le != cudaSuccess) return cuda_fail(le, "k_tconv launch");
     return B2C_OK;
 }
@@ -925,6 +997,7 @@ int wino_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
         a.tiles_m = p.tiles_m;
         a.units = (int)p.units;
         a.fCB = FastDiv(1u);
+        set_unit_divs(a);
         a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
         a.ws = reinterpret_cast<float*>(wsb + p.part_off);
         a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
@@ -1282,8 +1355,9 @@ int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t) {
         default: {
             const UmmaPlan p = umma_plan(d, t);
             if (!t->tma) return p.grid_x * p.grid_y * p.split;
-            const int occ = t->stages == 2 ? 2 : 1, cl = t->cluster >= 2 ? 2 : 1;
+            const int occ = t->stages == 2 ? 2 : 1, cl = (t->cluster == 2 || t->cluster == 3) ? 2 : 1;
             const int units = (cl == 2 ? (p.grid_x + 1) / 2 * p.grid_y : p.tiles) * p.split;
+            if (t->cluster == 4) return p.split * std::min(p.tiles, std::max(1, num_sms() / p.split));
             return p.streamk ? p.sk_grid : cl == 2 ? 2 * std::min(units, num_sms() / 2) : std::min(units, occ * num_sms());
         }
     }

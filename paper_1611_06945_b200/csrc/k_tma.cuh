@@ -76,6 +76,8 @@ constexpr int TM_MAX_SMEM = 232448;    // 227 KB opt-in per CTA
 constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 
 // PREC 0: fp32-exact 3xTF32 (kind::tf32, A = raw | lo in TMEM, B = packed raw | lo).
+// PREC 2: e4m3 operands, fp32 accumulate (kind::f8f6f4): as PREC 1 with one K = 32 MMA per
+//         K block; filters packed as e4m3 in the no-swizzle layout [16-element chunk][rows][16 B].
 // PREC 1: bf16 operands, fp32 accumulate (kind::f16): the split warps round the fp32
 //         pixel tile to bf16 into TMEM; filters are packed once as bf16 in the
 //         no-swizzle core-matrix layout [8-element chunk][rows][16 B].
@@ -85,11 +87,15 @@ constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 // filter tile (B rows) and its own 128 accumulator rows.
 template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
-    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && MODE != 7 && CL == 1), "bf16: pixels on M, packed filters");
+    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && MODE != 7 && CL == 1), "bf16 / fp8: pixels on M, packed filters");
     static constexpr bool RAW_B = MODE == 1 || MODE == 7;  // both operands raw [rows][K] matrices by TMA (no pack)
     static_assert((MODE != 5 && MODE != 6) || CL != 2, "MODE 5/6: no multicast pairs");
-    static_assert(CL == 1 || ((CL == 2 || CL == 3) && !SWAP && !RAW_B && OCC == 1), "pairs share B = packed filters");
+    static_assert(CL == 1 || CL == 4 || ((CL == 2 || CL == 3) && !SWAP && !RAW_B && OCC == 1), "pairs share B = packed filters");
+    static_assert(CL != 4 || OCC == 1, "cluster split-K: one CTA per SM (the staging tile)");
     static constexpr bool PAIR = CL == 3;  // 2-SM UMMA
+    static constexpr bool TWO_TILES = CL == 2 || CL == 3;  // a unit is two neighbouring pixel tiles
+    static constexpr bool CSPLIT = CL == 4;  // the split-K CTAs of a tile form one cluster; fixup over DSMEM
+    static constexpr int STG_BYTES = CSPLIT ? TM_M * BN * 4 : 0;  // this CTA's partial, [col][row] fp32
     static_assert(!PAIR || (BN >= 64 && BN <= 192), "2-SM UMMA: N = BN in [64, 192] (two accumulators + A slots in TMEM)");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
@@ -108,19 +114,20 @@ struct TmaCfg {
     static constexpr bool A_PRESPLIT = false;
     static constexpr bool B_SPLIT = SWAP || RAW_B;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
-    static constexpr int B_BYTES = PREC ? BN * 64 : (PAIR ? 1 : 2) * BN * 128;  // bf16 | raw + lo (a pair: half the rows each)
+    static constexpr int B_BYTES = PREC == 1 ? BN * 64 : PREC == 2 ? BN * 32 : (PAIR ? 1 : 2) * BN * 128;  // bf16 | e4m3 | raw + lo (a pair: half the rows each)
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
     static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
-    static constexpr int FLT_STAGE = PREC ? FLT_ROWS * 64 : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
+    static constexpr int FLT_STAGE = PREC == 1 ? FLT_ROWS * 64 : PREC == 2 ? FLT_ROWS * 32
+                                                                 : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
     static constexpr int FLT_HALF = FLT_ROWS / 2 * 128;   // 2-SM pair: one CTA's rows of one (raw | lo) image
     static constexpr int FLT_CTA = PAIR ? 2 * FLT_HALF : FLT_STAGE;  // filter bytes landing in one CTA per K block
     static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
     // OCC CTAs per SM share its 228 KB of shared memory (1 KB per CTA is the driver's) and 512 TMEM columns
-    static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024;
+    static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024 - STG_BYTES;
     static constexpr int SM_STAGES = BUDGET / STAGE_BYTES;
     static constexpr int STAGES = SM_STAGES < 8 ? SM_STAGES : 8;
-    static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES;
+    static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES + STG_BYTES;
     static constexpr int TMEM_COLS = OCC == 2 ? 256 : 512;
     // TMEM A stages (raw | lo: 64 columns each): as many as the columns left beside the two
     // accumulators allow (<= 4), so a split is not held up waiting for the MMAs of the stage
@@ -170,6 +177,9 @@ struct TArgs {
     // groups of 8 K (channel / window / K tail); the MMAs skip the all-zero rest.
     int kb_period, ksteps_last;
     int box_w;  // MODE 6: box width in floats (multiple of 4, >= bx + 3); the box is [32 ch][by][box_w]
+    // unit decomposition by multiply-shift (every role walks the units; no runtime integer divides
+    // on the loader's path to its first TMA)
+    FastDiv fSplit, fTilesN, fTilesMN, fPerImg, fTilesX;
 };
 
 // Walks a CTA's work: units blockIdx, +stride, ... ; or, in stream-K mode, the
@@ -185,17 +195,20 @@ __device__ __forceinline__ long long sk_start(long long W, int G, int c) { retur
 
 // Stream-K shares go to CTAs, or to CTA pairs (CL >= 2: both CTAs of a pair walk the same pair-units).
 template <int CL>
-__device__ __forceinline__ int sk_ctas() { return (int)gridDim.x / (CL >= 2 ? 2 : 1); }
+__device__ __forceinline__ int sk_ctas() { return (int)gridDim.x / ((CL == 2 || CL == 3) ? 2 : 1); }
 template <int CL>
-__device__ __forceinline__ int sk_me() { return (int)blockIdx.x / (CL >= 2 ? 2 : 1); }
+__device__ __forceinline__ int sk_me() { return (int)blockIdx.x / ((CL == 2 || CL == 3) ? 2 : 1); }
 
 template <int PIX_ROWS, int FLT_ROWS, int MODE, int CL>
 __device__ __forceinline__ UnitCursor cursor_begin(const TArgs& a, int ubase) {
     UnitCursor c;
     c.u = ubase;
-    const long long W = (long long)a.units * a.kblocks;
-    c.k = sk_start(W, sk_ctas<CL>(), sk_me<CL>());
-    c.end = sk_start(W, sk_ctas<CL>(), sk_me<CL>() + 1);
+    c.k = c.end = 0;
+    if (a.streamk) {
+        const long long W = (long long)a.units * a.kblocks;
+        c.k = sk_start(W, sk_ctas<CL>(), sk_me<CL>());
+        c.end = sk_start(W, sk_ctas<CL>(), sk_me<CL>() + 1);
+    }
     return c;
 }
 
@@ -211,27 +224,31 @@ struct Unit {
 template <int PIX_ROWS, int FLT_ROWS, int MODE, int CL = 1>
 __device__ __forceinline__ Unit unit_of(const TArgs& a, int u, int rank = 0) {
     Unit w;
-    w.z = u % a.split;
-    const int t2 = u / a.split;
+    uint32_t t2, zs;
+    a.fSplit.divmod((uint32_t)u, t2, zs);
+    w.z = (int)zs;
     // MODE 7: tile t2 of the batched GEMM = (z, pixel tile, filter tile), z outermost
-    const int zb = MODE == 7 ? t2 / (a.tiles_m * a.tiles_n) : 0;
-    const int t3 = MODE == 7 ? t2 - zb * (a.tiles_m * a.tiles_n) : t2;
-    const int nt = t3 % a.tiles_n;
-    const int mt = CL >= 2 ? 2 * (t3 / a.tiles_n) + rank : t3 / a.tiles_n;
+    uint32_t zb = 0, t3 = t2;
+    if (MODE == 7) a.fTilesMN.divmod(t2, zb, t3);
+    uint32_t mq, ntu;
+    a.fTilesN.divmod(t3, mq, ntu);
+    const int nt = (int)ntu;
+    const int mt = (CL == 2 || CL == 3) ? 2 * (int)mq + rank : (int)mq;
     w.ghost = mt >= a.tiles_m;
-    w.t = MODE == 7 ? t2 : mt * a.tiles_n + nt;
+    w.t = MODE == 7 ? (int)t2 : mt * a.tiles_n + nt;
     w.m0 = mt * PIX_ROWS;
     w.n0 = nt * FLT_ROWS;
     w.kb_begin = w.z * a.kps;
     w.nkb = min(a.kblocks, w.kb_begin + a.kps) - w.kb_begin;
     if (MODE == 4 || MODE == 5 || MODE == 6) {  // MODE 5: tiles_y = by = 1, bx = 128 (pixel runs of one image)
-        const int per_img = a.tiles_x * a.tiles_y;
-        w.b = mt / per_img;
-        const int r = mt - w.b * per_img;
-        w.oy0 = (r / a.tiles_x) * a.by;
-        w.ox0 = (r % a.tiles_x) * a.bx;
+        uint32_t b, r, ty, tx;
+        a.fPerImg.divmod((uint32_t)mt, b, r);
+        a.fTilesX.divmod(r, ty, tx);
+        w.b = (int)b;
+        w.oy0 = (int)ty * a.by;
+        w.ox0 = (int)tx * a.bx;
     } else {
-        w.b = zb;  // MODE 7: the GEMM's z (0 otherwise)
+        w.b = (int)zb;  // MODE 7: the GEMM's z (0 otherwise)
         w.oy0 = w.ox0 = 0;
     }
     w.nsplit = a.split;
@@ -493,6 +510,20 @@ __device__ __forceinline__ void a_to_tmem_bf16(uint32_t a, int tid, uint32_t tco
     tmem_st16u(tcol, r);
 }
 
+// fp8 mode: the same 32 fp32 of this thread's row as 32 e4m3 in 8 TMEM columns.
+template <bool SW128>
+__device__ __forceinline__ void a_to_tmem_e4m3(uint32_t a, int tid, uint32_t tcol) {
+    uint32_t r[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t off = SW128 ? (uint32_t)tid * 128u + (uint32_t)((c ^ (tid & 7)) * 16)
+                                   : (uint32_t)(c * TM_M * 16 + tid * 16);
+        const float4 q = lds128(a + off);
+        r[c] = pack_e4m3x4(q.x, q.y, q.z, q.w);
+    }
+    tmem_st8u(tcol, r);
+}
+
 // MODE 5 (1x1 convs read straight from NCHW): the TMA box is [32 channels][128
 // pixels] (no swizzle), so thread tid's row is a column of it: 32 scalar smem
 // loads at a 512-byte stride (consecutive threads hit consecutive banks).  PREC 0
@@ -507,6 +538,11 @@ __device__ __forceinline__ void a_to_tmem_cmajor(uint32_t a, int idx, uint32_t t
 #pragma unroll
         for (int j = 0; j < 16; ++j) r[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
         tmem_st16u(tcol, r);
+    } else if constexpr (PREC == 2) {
+        uint32_t r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = pack_e4m3x4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        tmem_st8u(tcol, r);
     } else {
         float l[32];
 #pragma unroll
@@ -524,16 +560,46 @@ __device__ __forceinline__ void a_to_tmem_cmajor(uint32_t a, int idx, uint32_t t
 // last for its tile (atomic ticket) reduces all partials in split order, so
 // results are deterministic.  Called by the NT drain threads; `row` is this
 // thread's TMEM lane (MMA M row), columns c_begin .. c_begin+DC.
-template <int BN, bool SWAP, int DC, int NT, int MODE>
+template <int BN, bool SWAP, int DC, int NT, int MODE, bool CSPLIT>
 __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, float* acc, int c_begin, int row,
-                                              int dtid, int* last_flag, float* bias_s, float bpre) {
+                                              int dtid, int* last_flag, float* bias_s, float bpre, uint32_t stg,
+                                              uint64_t* cs_bar, int& cs_uses) {
     const Geom& g = a.g;
     if (!SWAP) {  // the unit's out_chan biases -> smem (bpre was loaded by thread dtid before the drains)
         named_bar_sync(1, NT);  // previous unit's readers are done
         if (dtid < BN) bias_s[dtid] = bpre;
         named_bar_sync(1, NT);
     }
-    if (w.nsplit > 1) {
+    if (CSPLIT && w.nsplit > 1) {
+        // Cluster split-K: the tile's split CTAs are one thread-block cluster (rank = split
+        // index).  Each non-leader stages its partial in its own shared memory and signals
+        // the leader, which sums the partials over DSMEM in split order (deterministic),
+        // frees the peers' staging tiles and stores.  No global partials, no tickets.
+        const uint32_t rank = cluster_ctarank();
+        const int wl = threadIdx.x & 31;
+        if (rank != 0) {
+            if (cs_uses > 0) mbar_wait(smem_u32(&cs_bar[1]), (uint32_t)(cs_uses - 1) & 1u);
+#pragma unroll
+            for (int j = 0; j < DC; ++j) sts32(stg + (uint32_t)(((c_begin + j) * TM_M + row) * 4), acc[j]);
+            __syncwarp();
+            if (wl == 0) mbar_arrive_cluster(smem_u32(&cs_bar[0]), 0);
+            ++cs_uses;
+            return;
+        }
+        mbar_wait_cluster(smem_u32(&cs_bar[0]), (uint32_t)cs_uses & 1u);
+        for (int r = 1; r < w.nsplit; ++r) {
+            const uint32_t base = dsmem_addr(stg, (uint32_t)r);
+            float pv[DC];
+#pragma unroll
+            for (int j = 0; j < DC; ++j) pv[j] = ld_dsmem(base + (uint32_t)(((c_begin + j) * TM_M + row) * 4));
+#pragma unroll
+            for (int j = 0; j < DC; ++j) acc[j] += pv[j];
+        }
+        __syncwarp();
+        if (wl == 0)
+            for (int r = 1; r < w.nsplit; ++r) mbar_arrive_cluster_relaxed(smem_u32(&cs_bar[1]), (uint32_t)r);
+        ++cs_uses;
+    } else if (w.nsplit > 1) {
         // Split-K / stream-K fixup: every contributor publishes its fp32 partial
         // to L2, fences and takes a ticket; the one that arrives last reduces
         // all partials in split order (deterministic) and resets the ticket.
@@ -661,7 +727,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
     uint64_t* tempty_bar = tfull_bar + 2;      // [2]
     uint64_t* afree_bar = tempty_bar + 2;      // [A_SLOTS] TMEM A slot consumed by the MMAs
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afree_bar + Cfg::A_SLOTS);
+    uint64_t* cs_bar = afree_bar + Cfg::A_SLOTS;  // [2] cluster split-K: partials staged (leader), staging free (peers)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cs_bar + 2);
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* bias_s = reinterpret_cast<float*>(smem + 1024);
     const uint32_t tiles_u32 = (smem_u32(smem) + TM_HDR + 1023u) & ~1023u;
@@ -671,7 +738,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     const int warp = tid >> 5, lane = tid & 31;
     const int G = a.drain;
     const int rank = CL >= 2 ? (int)cluster_ctarank() : 0;
-    constexpr int NCTA = CL >= 2 ? 2 : 1;  // CTAs per cluster
+    constexpr int NCTA = Cfg::TWO_TILES ? 2 : 1;  // CTAs walking one unit sequence
     const int ubase = (int)blockIdx.x / NCTA, ustride = (int)gridDim.x / NCTA;
     if (tid == 0) B2C_TRACE(a.trace, 0);
 
@@ -686,6 +753,10 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
             mbar_init(smem_u32(&tempty_bar[s]), Cfg::DRAIN_ARRIVALS);
         }
         for (int s = 0; s < Cfg::A_SLOTS; ++s) mbar_init(smem_u32(&afree_bar[s]), 1);
+        if (Cfg::CSPLIT) {
+            mbar_init(smem_u32(&cs_bar[0]), (uint32_t)(a.split - 1) * (Cfg::DRAIN_THREADS / 32));
+            mbar_init(smem_u32(&cs_bar[1]), Cfg::DRAIN_THREADS / 32);
+        }
         mbar_fence_init();
     }
     if (warp == Cfg::MMA_WARP) {
@@ -743,6 +814,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 }
                 else if (PREC == 1)
                     a_to_tmem_bf16<Cfg::SW128>(sbase, tid, t_lane + acol);
+                else if (PREC == 2)
+                    a_to_tmem_e4m3<Cfg::SW128>(sbase, tid, t_lane + acol);
                 else if (!(a.trace & 8))
                     a_to_tmem<Cfg::SW128, Cfg::A_PRESPLIT>(sbase, tid, t_lane + acol);  // debug bit 3: skip
                 if (Cfg::B_SPLIT && !(a.trace & 4)) split_tile<BN>(sbase + Cfg::A_SMEM, tid);
@@ -773,6 +846,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
         const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c_begin;
         int ui = 0;  // unit ordinal (trace slots)
         int cidx = 0;
+        int cs_uses = 0;  // cluster split-K: units staged / reduced so far (barrier phases)
+        const uint32_t stg = tiles_u32 + (uint32_t)(STAGES * Cfg::STAGE_BYTES);  // staging tile (CSPLIT)
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
         for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
             float acc[DC];
@@ -797,14 +872,15 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
             if (dtid == 0 && ui == 0) B2C_TRACE(a.trace, 4);
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 208 + 2 * ui);
             if (!w.ghost)
-                epilogue_unit<BN, SWAP, DC, Cfg::DRAIN_THREADS, MODE>(a, w, acc, c_begin, row, dtid, last_flag, bias_s, bpre);
+                epilogue_unit<BN, SWAP, DC, Cfg::DRAIN_THREADS, MODE, Cfg::CSPLIT>(a, w, acc, c_begin, row, dtid, last_flag,
+                                                                                 bias_s, bpre, stg, cs_bar, cs_uses);
             if (dtid == 0 && ui < 24) B2C_TRACE(a.trace, 209 + 2 * ui);
             ++ui;
         }
         if (dtid == 0) B2C_TRACE(a.trace, 6);
     } else if (warp == Cfg::MMA_WARP && (!Cfg::PAIR || rank == 0)) {
         // ------------------------------------------------------------ MMA issuer (whole warp waits, one lane issues)
-        constexpr uint32_t idesc = umma_idesc(PREC == 1 ? 1 : 2, Cfg::PAIR ? 2 * TM_M : TM_M, BN);
+        constexpr uint32_t idesc = umma_idesc(PREC == 1 ? 1 : PREC == 2 ? 0 : 2, Cfg::PAIR ? 2 * TM_M : TM_M, BN);
         int stage = 0, cidx = 0, n = 0;
         uint32_t phase = 0;
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
@@ -838,7 +914,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
                     const uint32_t b_lo = b_raw + (Cfg::PAIR ? BN / 2 : BN) * 128;
                     const uint32_t d = tmem_base + (uint32_t)(slot * BN);
-                    if constexpr (PREC == 1) {  // bf16: two K=16 MMAs per 32-wide K block
+                    if constexpr (PREC == 2) {  // e4m3: one K=32 MMA per K block ([2 chunks][rows][16 B])
+                        mma_e4m3_ts(d, a_hi, umma_desc(b_raw, BN * 16, 128), idesc, first ? 0u : 1u);
+                    } else if constexpr (PREC == 1) {  // bf16: two K=16 MMAs per 32-wide K block
 #pragma unroll
                         for (int s = 0; s < TM_BK / 16; ++s) {
                             if (2 * s >= nsteps) break;

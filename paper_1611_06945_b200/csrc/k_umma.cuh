@@ -282,6 +282,28 @@ __global__ void __launch_bounds__(256) k_pack_filters_bf16(Geom g, const float* 
     }
 }
 
+// e4m3 pack for the TMA kernel's fp8 mode: [filter tile][K block][16-element chunk 0..1][rows][16 x e4m3]
+// (UMMA no-swizzle K-major core matrices: 8 rows x 16 B contiguous), round to nearest even, saturating.
+__global__ void __launch_bounds__(256) k_pack_filters_e4m3(Geom g, const float* __restrict__ w,
+                                                           uint8_t* __restrict__ out, int rows, int kblocks,
+                                                           FastDiv fCB, int kmode, long long total) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)(i & 15);
+        long long t = i >> 4;
+        const int r = (int)(t % rows);
+        t /= rows;
+        const int c = (int)(t & 1);
+        t >>= 1;
+        const int kb = (int)(t % kblocks);
+        const int tile = (int)(t / kblocks);
+        const float v = packed_k_value(g, w, tile * rows + r, kb, 16 * c + e, fCB, kmode);
+        uint16_t two;
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(two) : "f"(0.0f), "f"(v));
+        out[i] = (uint8_t)(two & 0xFF);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __restrict__ w, float* __restrict__ out,
                                                       int rows, int kblocks, FastDiv fCB, int kmode,
                                                       long long total, int swz, int parts) {

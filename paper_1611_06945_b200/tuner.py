@@ -82,6 +82,7 @@ class ToleranceSpec:
 
 
 BF16_REL_TOL = 4e-3  # bf16 operands, fp32 accumulate
+FP8_REL_TOL = 0.13  # e4m3 operands: <= 2*2^-4 + 2^-8 relative per product (rigorous on U[0.1, 1) data), fp32 accumulate
 
 
 def tolerance_for(reduction_terms: int, prec: int = 0) -> ToleranceSpec:
@@ -89,6 +90,8 @@ def tolerance_for(reduction_terms: int, prec: int = 0) -> ToleranceSpec:
     separately stated bf16-mode tolerance is rel 4e-3."""
     if prec == 1:
         return ToleranceSpec(rel_tol=BF16_REL_TOL)
+    if prec == 2:
+        return ToleranceSpec(rel_tol=FP8_REL_TOL)
     return ToleranceSpec(rel_tol=1e-3) if reduction_terms > LONG_REDUCTION_TERMS else ToleranceSpec()
 
 

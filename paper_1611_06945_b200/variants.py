@@ -280,6 +280,8 @@ class _UmmaFamily(Variant):
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
                         if tma in (1, 3, 4) and bn in (64, 128, 192) and not swap:  # 2-SM UMMA pairs (M = 256)
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=3))
+                        if 2 <= split <= 8 and tma in (1, 3, 4) and (bn in (32, 64) and not swap or bn == 32 and swap):
+                            out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=4))  # split-K cluster
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

@@ -67,7 +67,9 @@ def _variant_params(g):
                     TuneParams(bn=128, split_k=2, tma=1, cl=3), TuneParams(bn=192, tma=1, cl=3),
                     TuneParams(bn=128, tma=4, cl=3), TuneParams(bn=64, split_k=2, tma=3, cl=3),
                     TuneParams(bn=128, tma=3, cl=3), TuneParams(bn=128, split_k=0, tma=1, cl=3),
-                    TuneParams(bn=64, split_k=0, tma=4, cl=3)):
+                    TuneParams(bn=64, split_k=0, tma=4, cl=3), TuneParams(bn=32, split_k=2, tma=1, cl=4),
+                    TuneParams(bn=64, split_k=4, tma=1, cl=4), TuneParams(bn=32, split_k=3, tma=3, cl=4),
+                    TuneParams(bn=64, split_k=2, tma=4, cl=4), TuneParams(bn=32, swap_ab=True, split_k=4, tma=1, cl=4)):
             out.append((v, prm))
     out += [("conv_wino", p) for p in (TuneParams(bn=64, tma=1), TuneParams(bn=128, split_k=2, tma=1),
                                        TuneParams(bn=192, split_k=0, tma=1), TuneParams(bn=64, swap_ab=True, tma=1),
