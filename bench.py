@@ -69,7 +69,7 @@ CONFIG3_ROWS = (2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 14, 18, 19)
 def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--batches", default="1,5,20")
