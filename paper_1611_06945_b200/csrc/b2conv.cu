@@ -95,6 +95,7 @@ bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || 
 int window_chunks(const b2c_conv_desc* d) { return (d->r * 4 + TM_BK - 1) / TM_BK; }
 int kmode_for(const b2c_conv_desc* d, int variant, int tma) {
     if (variant == B2C_VAR_FC) return 2;
+    if (tma == 5) return 6;  // bf16 NHWC copy: (tap, 64-channel block) per K block, SS MMAs
     if (tma && tma != 3 && tma != 4 && d->c <= 4) return tma == 2 ? 4 : 5;
     if (variant == B2C_VAR_1X1 || tma) return 3;
     return d->c >= 32 ? 3 : 0;
@@ -104,6 +105,7 @@ int kblocks_for(const b2c_conv_desc* d, int kmode) {
     if (kmode == 4) return (d->r * d->r + TM_TAPS - 1) / TM_TAPS;
     if (kmode == 5) return d->r * window_chunks(d);
     if (kmode == 3) return d->r * d->r * ((d->c + 31) / 32);
+    if (kmode == 6) return d->r * d->r * ((d->c + 63) / 64);
     return (d->c * d->r * d->r + 31) / 32;
 }
 
@@ -220,7 +222,16 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K: single CTAs or 2-SM pairs"; return B2C_INAPPLICABLE; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
-    if (t->tma < 0 || t->tma > 4) { why = "tma must be 0..4"; return B2C_BAD_ARGS; }
+    if (t->tma < 0 || t->tma > 5) { why = "tma must be 0..5"; return B2C_BAD_ARGS; }
+    if (t->tma == 5) {  // bf16 mode: bf16 NHWC copy + SS MMAs (MODE 8)
+        if (d->prec != B2C_PREC_BF16) { why = "tma=5 is the bf16 mode's NHWC-bf16 / SS-MMA path"; return B2C_INAPPLICABLE; }
+        if (t->variant == B2C_VAR_FC || t->swap_ab || t->cluster >= 2 || t->stages == 2) {
+            why = "tma=5: a conv variant, pixels on M, single CTAs, 1 CTA/SM"; return B2C_INAPPLICABLE;
+        }
+        if (d->c % 8 || d->c <= 4) { why = "tma=5 needs in_chans % 8 == 0 (16-byte bf16 NHWC pixels)"; return B2C_INAPPLICABLE; }
+        if (t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) { why = "tma=5: tile_n in {64, 128, 192}"; return B2C_INAPPLICABLE; }
+        if (t->split_k < 0) { why = "split_k must be >= 0"; return B2C_BAD_ARGS; }
+    }
     if (t->tma == 4) {  // k x k stride-1 conv read straight from NCHW x (no re-layout launch)
         if (d->stride != 1 || d->r < 2 || t->variant == B2C_VAR_FC) {
             why = "tma=4 (direct NCHW k x k) needs a stride-1 conv with ksz >= 2"; return B2C_INAPPLICABLE;
@@ -301,7 +312,7 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.tma = t->tma;
     p.kmode = kmode_for(d, t->variant, t->tma);
     p.kblocks = kblocks_for(d, p.kmode);
-    p.cblocks = p.kmode == 5 ? window_chunks(d) : (d->c + 31) / 32;
+    p.cblocks = p.kmode == 5 ? window_chunks(d) : p.kmode == 6 ? (d->c + 63) / 64 : (d->c + 31) / 32;
     p.bx = p.by = p.tiles_x = p.tiles_y = p.hp = p.wp = p.box_w = 0;
     if (t->tma == 4) {  // MODE 6: whole output rows of one image, the box 3+ floats wider for the aligned start
         p.bx = d->ow;
@@ -335,7 +346,7 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.split = (p.kblocks + p.kps - 1) / p.kps;  // every split gets >= 1 block
     // packed filters: raw | lo per K block; raw only when the TMA kernel takes them as its TMEM A operand
     p.parts = (p.tma && t->swap_ab) || d->prec != B2C_PREC_FP32 ? 1 : 2;
-    const size_t row_bytes = d->prec == B2C_PREC_BF16 ? UMMA_BK * 2 : d->prec == B2C_PREC_FP8 ? UMMA_BK
+    const size_t row_bytes = p.kmode == 6 ? 128 : d->prec == B2C_PREC_BF16 ? UMMA_BK * 2 : d->prec == B2C_PREC_FP8 ? UMMA_BK
                                                                                            : UMMA_BK * sizeof(float);  // per K block
     p.wpk_bytes = (p.tma && p.kmode == 2) ? 0 : (size_t)p.grid_y * p.kblocks * p.parts * p.flt_rows * row_bytes;
     p.streamk = (t->tma && t->split_k == 0) ? 1 : 0;
@@ -355,10 +366,11 @@ UmmaPlan umma_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     p.part_off = align256(p.wpk_bytes);
     p.sems_off = p.part_off + (nslots ? align256(nslots * BN * UMMA_M * sizeof(float)) : 0);
     p.nhwc_off = p.sems_off + (nslots ? align256((size_t)p.tiles * sizeof(int)) : 0);
-    const bool nhwc = p.tma && p.tma != 3 && p.tma != 4 && (p.kmode == 3 || p.kmode == 4 || p.kmode == 5);
-    const int cp = p.kmode >= 4 ? 4 : d->c;  // first layers: channels padded to 4 (16-byte pixels)
+    const bool nhwc = p.tma && p.tma != 3 && p.tma != 4 && (p.kmode == 3 || p.kmode == 4 || p.kmode == 5 || p.kmode == 6);
+    const int cp = (p.kmode == 4 || p.kmode == 5) ? 4 : d->c;  // first layers: channels padded to 4 (16-byte pixels)
     const size_t pix = p.kmode == 5 ? (size_t)p.hp * p.wp : (size_t)d->h * d->w;
-    p.gbar_off = p.nhwc_off + (nhwc ? align256((size_t)d->n * cp * pix * sizeof(float)) : 0);
+    const size_t elt = p.kmode == 6 ? 2 : sizeof(float);  // kmode 6: bf16 NHWC copy
+    p.gbar_off = p.nhwc_off + (nhwc ? align256((size_t)d->n * cp * pix * elt) : 0);
     p.ws_bytes = p.gbar_off + (p.tma ? 256 : 0);  // grid-barrier counter of the fused re-layout
     return p;
 }
@@ -412,6 +424,13 @@ int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* w
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
         k_pack_filters_e4m3<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<uint8_t*>(ws), p.flt_rows, p.kblocks,
                                                     FastDiv((uint32_t)p.cblocks), p.kmode, total);
+        return B2C_OK;
+    }
+    if (p.kmode == 6) {  // bf16 SW128 images of (tap, 64-channel block) for the SS MMAs
+        const long long total = (long long)p.wpk_bytes / 2;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+        k_pack_filters_bf16_sw128<<<blocks, 256, 0, st>>>(g, w, reinterpret_cast<uint16_t*>(ws), p.flt_rows, p.kblocks,
+                                                          FastDiv((uint32_t)p.cblocks), total);
         return B2C_OK;
     }
     if (d->prec == B2C_PREC_BF16) {
@@ -514,18 +533,20 @@ void im2col_small_tensor_fix(CUtensorMap* tm, size_t tensor_bytes) {
 // NHWC tensor (cp channels per pixel) for im2col loads of `pix_rows` output
 // pixels x `cpp` channels; the bounding box corners are the conv padding
 // (lower = -pad, upper = pad - (ksz - 1)), the traversal strides the conv stride.
-int encode_im2col(CUtensorMap* tm, const b2c_conv_desc* d, const float* xh, int cp, int cpp, int pix_rows, bool sw128) {
+int encode_im2col(CUtensorMap* tm, const b2c_conv_desc* d, const void* xh, int cp, int cpp, int pix_rows, bool sw128,
+                  int elt = 4) {
     const cuuint64_t dims[4] = {(cuuint64_t)cp, (cuuint64_t)d->w, (cuuint64_t)d->h, (cuuint64_t)d->n};
-    const cuuint64_t strides[3] = {(cuuint64_t)cp * 4, (cuuint64_t)d->w * cp * 4, (cuuint64_t)d->h * d->w * cp * 4};
+    const cuuint64_t strides[3] = {(cuuint64_t)cp * elt, (cuuint64_t)d->w * cp * elt, (cuuint64_t)d->h * d->w * cp * elt};
     const int lower[2] = {-d->pad, -d->pad};
     const int upper[2] = {d->pad - (d->r - 1), d->pad - (d->r - 1)};
     const cuuint32_t estr[4] = {1, (cuuint32_t)d->stride, (cuuint32_t)d->stride, 1};
-    CUresult r = g_enc_im2col(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(xh), dims, strides, lower,
+    CUresult r = g_enc_im2col(tm, elt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                              const_cast<void*>(xh), dims, strides, lower,
                               upper, (cuuint32_t)cpp, (cuuint32_t)pix_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                               sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(B2C_CUDA_ERROR, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
-    im2col_small_tensor_fix(tm, (size_t)d->n * cp * d->h * d->w * 4);
+    im2col_small_tensor_fix(tm, (size_t)d->n * cp * d->h * d->w * elt);
     return B2C_OK;
 }
 
@@ -719,7 +740,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     int rc = load_tma_encoders();
     if (rc) return rc;
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
-    const int mode = t->tma == 4 ? 6 : t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
+    const int mode = t->tma == 5 ? 8 : t->tma == 4 ? 6 : t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
     const int cl = (t->cluster >= 2 && t->cluster <= 4) ? t->cluster : 1;
     TconvEntry e{nullptr, 0, 0};
@@ -727,6 +748,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
             : mode == 4 ? tconv_pick_bf16<4>(t->tile_n) : mode == 5 ? tconv_pick_bf16<5>(t->tile_n)
             : mode == 6 ? tconv_pick_bf16<6>(t->tile_n)
+            : mode == 8 ? tconv_pick_bf16<8>(t->tile_n)
             : TconvEntry{nullptr, 0, 0};
     else if (d->prec == B2C_PREC_FP8)
         e = mode == 0 ? tconv_pick_fp8<0>(t->tile_n) : mode == 4 ? tconv_pick_fp8<4>(t->tile_n)
@@ -773,6 +795,16 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
             if (le != cudaSuccess) return cuda_fail(le, "k_to_nhwc4_pad launch");
         }
         rc = encode_window(&tm_pix, d, p, xp);
+        if (rc) return rc;
+    } else if (mode == 8) {  // bf16 NHWC copy, im2col boxes of 128 pixels x 64 channels (128-byte rows)
+        uint16_t* xb = reinterpret_cast<uint16_t*>(wsb + p.nhwc_off);
+        const int HW = d->h * d->w;
+        if (!(g_trace_on & 16)) {
+            dim3 tgrid((HW + 31) / 32, (d->c + 31) / 32, d->n);
+            cudaError_t le = launch_pdl(k_nchw_to_nhwc_bf16, tgrid, dim3(256), 0, st, 1, x, xb, (int)d->c, HW);
+            if (le != cudaSuccess) return cuda_fail(le, "bf16 NHWC conversion launch");
+        }
+        rc = encode_im2col(&tm_pix, d, xb, d->c, 64, pix_rows, true, 2);
         if (rc) return rc;
     } else if (mode != 1) {
         float* xh = reinterpret_cast<float*>(wsb + p.nhwc_off);
@@ -837,7 +869,10 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.flt_early = t->prepared ? 1 : 0;  // b2c_conv_prepare synchronises, so a prepared pack is complete
     {
         int period = p.kblocks, valid = g.K - TM_BK * (p.kblocks - 1);  // fc (MODE 1): flat K tail
-        if (mode == 0 || mode == 2 || mode == 5 || mode == 6) {
+        if (mode == 8) {  // 64-channel blocks, K = 16 per MMA step
+            period = p.cblocks;
+            valid = (d->c - 64 * (period - 1) + 1) / 2;  // ceil(valid / 8) below = ceil(channels / 16) MMA steps
+        } else if (mode == 0 || mode == 2 || mode == 5 || mode == 6) {
             period = p.cblocks;
             valid = d->c - TM_BK * (period - 1);
         } else if (mode == 4) {

@@ -29,6 +29,11 @@
 //     pixels x 32 window floats per box into the SWIZZLE_128B layout: 128-byte
 //     rows instead of MODE 3's 16-byte ones (the TMA unit issues ~0.75 rows
 //     per clock per SM, so row width sets its throughput).
+//   * MODE 8 (bf16 mode, tm=5): x re-laid out to a bf16 NHWC copy; one im2col TMA
+//     per K block brings 128 output pixels x 64 bf16 channels of one filter tap
+//     (128-byte rows, SWIZZLE_128B) and the filters are packed once as bf16 in the
+//     same layout, so both MMA operands come straight from shared memory (SS
+//     kind::f16 MMAs, four K = 16 steps per block): no split pass at all.
 //   * MODE 7 (Winograd F(2x2,3x3), conv_wino): 16 independent GEMMs
 //     M[z] = V[z] * U[z]^T over the transformed tiles (k_wino.cuh): MODE 1 with a
 //     third TMA coordinate z, no bias / activation (the output transform adds them).
@@ -89,6 +94,8 @@ template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
     static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && MODE != 7 && CL == 1), "bf16 / fp8: pixels on M, packed filters");
     static constexpr bool RAW_B = MODE == 1 || MODE == 7;  // both operands raw [rows][K] matrices by TMA (no pack)
+    static constexpr bool SS = MODE == 8;  // bf16 NHWC copy: A and B straight from shared memory, no split pass
+    static_assert(!SS || (PREC == 1 && !SWAP && CL == 1 && OCC == 1), "MODE 8: bf16, pixels on M, single CTAs");
     static_assert((MODE != 5 && MODE != 6) || CL != 2, "MODE 5/6: no multicast pairs");
     static_assert(CL == 1 || CL == 4 || ((CL == 2 || CL == 3) && !SWAP && !RAW_B && OCC == 1), "pairs share B = packed filters");
     static_assert(CL != 4 || OCC == 1, "cluster split-K: one CTA per SM (the staging tile)");
@@ -104,8 +111,12 @@ struct TmaCfg {
     static constexpr int DRAIN_COLS = BN / DG;
     static constexpr int DRAIN_THREADS = 128 * DG;
     static constexpr int MMA_WARP = 4 + 4 * DG;
-    static constexpr int LOAD_WARP = MMA_WARP + 1;
-    static constexpr int THREADS = 32 * (LOAD_WARP + 1);
+    static constexpr int LOAD_WARP = MMA_WARP + 1;  // pixel / activation tiles (one TMA per stage: ~200 issue cycles)
+    // filter stages from their own warp, issued in parallel with the pixel loads; with two CTAs
+    // per SM the extra warp would cost registers the drain warps need, so one warp issues both
+    static constexpr bool TWO_LOADERS = OCC == 1;
+    static constexpr int FLT_WARP = TWO_LOADERS ? LOAD_WARP + 1 : LOAD_WARP;
+    static constexpr int THREADS = 32 * (FLT_WARP + 1);
     static constexpr int PIX_ROWS = SWAP ? BN : TM_M;
     static constexpr int FLT_ROWS = SWAP ? TM_M : BN;
     // The MMA's A operand (M = 128 rows) lives in TMEM: the split warps move
@@ -114,11 +125,12 @@ struct TmaCfg {
     static constexpr bool A_PRESPLIT = false;
     static constexpr bool B_SPLIT = SWAP || RAW_B;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
-    static constexpr int B_BYTES = PREC == 1 ? BN * 64 : PREC == 2 ? BN * 32 : (PAIR ? 1 : 2) * BN * 128;  // bf16 | e4m3 | raw + lo (a pair: half the rows each)
+    static constexpr int B_BYTES = SS ? BN * 128 : PREC == 1 ? BN * 64 : PREC == 2 ? BN * 32
+                                                             : (PAIR ? 1 : 2) * BN * 128;  // bf16 SW128 64-K | bf16 | e4m3 | raw + lo (a pair: half the rows each)
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
     static constexpr int FLT_OFF = SWAP ? 0 : A_SMEM;
-    static constexpr int FLT_STAGE = PREC == 1 ? FLT_ROWS * 64 : PREC == 2 ? FLT_ROWS * 32
+    static constexpr int FLT_STAGE = SS ? FLT_ROWS * 128 : PREC == 1 ? FLT_ROWS * 64 : PREC == 2 ? FLT_ROWS * 32
                                                                  : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
     static constexpr int FLT_HALF = FLT_ROWS / 2 * 128;   // 2-SM pair: one CTA's rows of one (raw | lo) image
     static constexpr int FLT_CTA = PAIR ? 2 * FLT_HALF : FLT_STAGE;  // filter bytes landing in one CTA per K block
@@ -137,6 +149,7 @@ struct TmaCfg {
     static_assert(ACC_COLS + A_SLOTS * 64 <= TMEM_COLS, "TMEM budget");
     static constexpr bool SW128 = MODE != 3;
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (RAW_B ? FLT_ROWS * 128 : FLT_CTA);
+    static constexpr uint32_t FLT_BYTES = RAW_B ? FLT_ROWS * 128 : FLT_CTA;  // the filter warp's bytes per stage
     // barrier arrival counts (a pair's leader counts its peer's split / drain warps too)
     static constexpr int SPLIT_ARRIVALS = PAIR ? 2 * (TM_SPLIT_THREADS / 32) : TM_SPLIT_THREADS;
     static constexpr int DRAIN_ARRIVALS = PAIR ? 2 * (DRAIN_THREADS / 32) : DRAIN_THREADS;
@@ -313,6 +326,31 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
     for (int j = ty; j < 32; j += 8) {
         const int p = p0 + j, c = c0 + tx;
         if (p < HW && c < Cp) dst[(size_t)p * Cp + c] = tile[tx][j];
+    }
+}
+
+// bf16 mode, MODE 8: x [N][C][HW] fp32 -> xh [N][HW][C] bf16 (round to nearest even, the
+// rounding the split pass of the TS path applies); same 32x32 smem tiles, 2-byte stores.
+__global__ void __launch_bounds__(256) k_nchw_to_nhwc_bf16(const float* __restrict__ x, uint16_t* __restrict__ xh,
+                                                           int C, int HW) {
+    __shared__ float tile[32][33];
+    pdl_launch_dependents();
+    pdl_wait();
+    const int n = blockIdx.z;
+    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const float* src = x + (size_t)n * C * HW;
+    uint16_t* dst = xh + (size_t)n * HW * C;
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+        const int c = c0 + j, p = p0 + tx;
+        tile[j][tx] = (c < C && p < HW) ? __ldg(src + (size_t)c * HW + p) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+        const int p = p0 + j, c = c0 + tx;
+        if (p < HW && c < C) dst[(size_t)p * C + c] = (uint16_t)(pack_bf16x2(tile[tx][j], 0.0f) & 0xFFFFu);
     }
 }
 
@@ -744,7 +782,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(smem_u32(&raw_full[s]), 1);
+            mbar_init(smem_u32(&raw_full[s]), Cfg::TWO_LOADERS ? 2 : 1);  // each loader arrives with its bytes
             mbar_init(smem_u32(&split_full[s]), Cfg::SPLIT_ARRIVALS);
             mbar_init(smem_u32(&empty_bar[s]), CL == 2 ? 2 : 1);  // one tcgen05.commit per MMA-issuing CTA
         }
@@ -779,13 +817,14 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     // The loader may stream the first stages' packed filters (constant, written
     // by an earlier synchronised b2c_conv_prepare) while the previous kernel
     // (the x re-layout) is still running; everything else waits for it here.
-    const bool early = a.flt_early && !Cfg::RAW_B && !a.relayout && warp == Cfg::LOAD_WARP;
+    const bool early = Cfg::TWO_LOADERS && a.flt_early && !Cfg::RAW_B && !a.relayout && warp == Cfg::FLT_WARP;
     if (!early) pdl_wait();
     if (a.relayout) fused_relayout(a, smem + TM_HDR + 1024);
     if (tid == 0) B2C_TRACE(a.trace, 3);
 
     if (warp < 4) {
         // ------------------------------------------------------------ split: A -> TMEM (raw | lo), B lo -> smem
+        if constexpr (!Cfg::SS) {  // MODE 8: the MMAs read both operands from shared memory (no split)
         int stage = 0, n = 0;
         uint32_t phase = 0;
         const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);  // this warp's 32 TMEM lanes
@@ -835,6 +874,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     phase ^= 1u;
                 }
             }
+        }
         }
     } else if (warp < Cfg::MMA_WARP) {
         // ------------------------------------------------------------ drain + epilogue
@@ -904,6 +944,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 // raw_full, so it also covers the TMA / bulk bytes (a pair: both CTAs').
                 if (Cfg::PAIR)
                     mbar_wait_cluster(smem_u32(&split_full[stage]), phase);
+                else if (Cfg::SS)  // no split pass: wait for the TMA / bulk bytes themselves
+                    mbar_wait(smem_u32(&raw_full[stage]), phase);
                 else
                     mbar_wait(smem_u32(&split_full[stage]), phase);
                 tc_fence_after();
@@ -914,7 +956,15 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
                     const uint32_t b_lo = b_raw + (Cfg::PAIR ? BN / 2 : BN) * 128;
                     const uint32_t d = tmem_base + (uint32_t)(slot * BN);
-                    if constexpr (PREC == 2) {  // e4m3: one K=32 MMA per K block ([2 chunks][rows][16 B])
+                    if constexpr (Cfg::SS) {  // bf16 SS: four K = 16 MMAs per 64-wide K block, +32 B per step
+                        const uint32_t a_s = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::PIX_OFF);
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            if (s >= nsteps) break;  // all-zero channel tail
+                            mma_bf16(d, umma_desc_sw128(a_s + s * 32), umma_desc_sw128(b_raw + s * 32), idesc,
+                                     (first && s == 0) ? 0u : 1u);
+                        }
+                    } else if constexpr (PREC == 2) {  // e4m3: one K=32 MMA per K block ([2 chunks][rows][16 B])
                         mma_e4m3_ts(d, a_hi, umma_desc(b_raw, BN * 16, 128), idesc, first ? 0u : 1u);
                     } else if constexpr (PREC == 1) {  // bf16: two K=16 MMAs per 32-wide K block
 #pragma unroll
@@ -979,7 +1029,91 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
         }
         if (lane == 0) B2C_TRACE(a.trace, 5);
     } else if (warp == Cfg::LOAD_WARP && lane == 0) {
-        // ------------------------------------------------------------ TMA / bulk loader
+        // ------------------------------------------------------------ pixel / activation loader (TMA)
+        // (with one loader warp, OCC == 2, it issues each stage's filters too; the early filter
+        // prefetch is then off)
+        int stage = 0, n = 0;
+        uint32_t phase = 0;
+        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
+            int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
+            if (MODE == 0 || MODE == 3 || MODE == 8) {
+                uint32_t b, p, oy, ox;
+                g.fPQ.divmod((uint32_t)w.m0, b, p);
+                g.fOW.divmod(p, oy, ox);
+                pw = (int)ox * g.S - g.P;
+                ph = (int)oy * g.S - g.P;
+                pn = (int)b;
+            }
+            for (int i = 0; i < w.nkb; ++i, ++n) {
+                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
+                const uint32_t bar = smem_u32(&raw_full[stage]);
+                const uint32_t pix = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::PIX_OFF;
+                const int kb = w.kb_begin + i;
+                // MODE 4 / 6 boxes are bx*by / box_w*by rows (<= 128): the rest of the tile keeps
+                // stale (finite) data whose output rows the epilogue discards.
+                const uint32_t bytes = (MODE == 4   ? (uint32_t)(a.bx * a.by) * 128u
+                                        : MODE == 6 ? (uint32_t)(a.box_w * a.by) * 128u
+                                                    : (uint32_t)Cfg::PIX_ROWS * 128u) +
+                                       (Cfg::TWO_LOADERS ? 0u : Cfg::FLT_BYTES);
+                mbar_arrive_expect_tx(bar, bytes);
+                if (!Cfg::TWO_LOADERS) {
+                    const uint32_t dst = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::FLT_OFF;
+                    if (MODE == 1)
+                        tma_load_2d(dst, &tm_flt, bar, kb * TM_BK, w.n0);
+                    else if (MODE == 7)
+                        tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
+                    else
+                        load_filters<Cfg::FLT_STAGE, CL>(
+                            dst, reinterpret_cast<const char*>(a.wpk) +
+                                     ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + kb) * (size_t)Cfg::FLT_STAGE, bar, rank);
+                }
+                if (n < 32) B2C_TRACE(a.trace, 176 + n);
+                if (MODE == 1 || MODE == 2) {
+                    tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
+                } else if (MODE == 7) {  // V[z] rows: (k, row, z)
+                    tma_load_3d(pix, &tm_pix, bar, kb * TM_BK, w.m0, w.b);
+                } else if (MODE == 5) {  // (pixel run, channel block, image) straight from NCHW x
+                    tma_load_3d(pix, &tm_pix, bar, w.ox0, kb * TM_BK, w.b);
+                } else if (MODE == 6) {  // (x, y, channel block, image) of NCHW x; x start rounded down to 16 B
+                    uint32_t tap, cb, ky, kx;
+                    a.fCB.divmod((uint32_t)kb, tap, cb);
+                    g.fR.divmod(tap, ky, kx);
+                    const int dx = w.ox0 + (int)kx - g.P;
+                    const int xs = ((dx >= 0 ? dx : dx - 3) / 4) * 4;  // floor to a multiple of 4 floats
+                    tma_load_4d(pix, &tm_pix, bar, xs, w.oy0 + (int)ky - g.P, (int)cb * TM_BK, w.b);
+                } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
+                    uint32_t ky, kc;
+                    a.fCB.divmod((uint32_t)kb, ky, kc);
+                    tma_load_5d(pix, &tm_pix, bar, (int)kc * TM_BK, w.ox0, w.oy0, (int)ky, w.b);
+                } else if (MODE == 0 || MODE == 8) {  // MODE 8: 64 bf16 channels per block
+                    uint32_t tap, cb, ky, kx;
+                    a.fCB.divmod((uint32_t)kb, tap, cb);
+                    g.fR.divmod(tap, ky, kx);
+                    tma_load_im2col_4d(pix, &tm_pix, bar, (int)cb * (MODE == 8 ? 64 : TM_BK), pw, ph, pn, (uint16_t)kx,
+                                       (uint16_t)ky);
+                } else {  // MODE 3: 8 taps x 4 channels, one 16-byte-pixel box per tap
+#pragma unroll 1
+                    for (int j = 0; j < TM_TAPS; ++j) {
+                        const int tap = kb * TM_TAPS + j;
+                        uint32_t ky = 0, kx = 0;
+                        int c = 4;  // taps past R*R: channel 4 is out of bounds -> zeros
+                        if (tap < g.RR) {
+                            g.fR.divmod((uint32_t)tap, ky, kx);
+                            c = 0;
+                        }
+                        tma_load_im2col_4d(pix + (uint32_t)(j * Cfg::PIX_ROWS * 16), &tm_pix, bar, c, pw, ph, pn,
+                                           (uint16_t)kx, (uint16_t)ky);
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (Cfg::TWO_LOADERS && warp == Cfg::FLT_WARP && lane == 0) {
+        // ------------------------------------------------------------ filter loader (bulk copies / TMA)
         int stage = 0, n = 0;
         uint32_t phase = 0;
         int npre = 0;  // stages whose filter bytes were issued before griddepcontrol.wait
@@ -990,9 +1124,9 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 npre = min(STAGES, w0.nkb);
                 const char* wsrc0 = reinterpret_cast<const char*>(a.wpk) +
                                     ((size_t)(w0.n0 / Cfg::FLT_ROWS) * a.kblocks + w0.kb_begin) * (size_t)Cfg::FLT_STAGE;
-                for (int i = 0; i < npre; ++i) {
+                for (int i = 0; i < npre; ++i) {  // fresh stages: no empty wait
                     const uint32_t bar = smem_u32(&raw_full[i]);
-                    mbar_expect_tx(bar, Cfg::FLT_CTA);
+                    mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
                     load_filters<Cfg::FLT_STAGE, CL>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
                                                     wsrc0 + (size_t)i * Cfg::FLT_STAGE, bar, rank);
                 }
@@ -1003,74 +1137,21 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
         }
         UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
         for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
-            int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
-            if (MODE == 0 || MODE == 3) {
-                uint32_t b, p, oy, ox;
-                g.fPQ.divmod((uint32_t)w.m0, b, p);
-                g.fOW.divmod(p, oy, ox);
-                pw = (int)ox * g.S - g.P;
-                ph = (int)oy * g.S - g.P;
-                pn = (int)b;
-            }
             const char* wsrc = reinterpret_cast<const char*>(a.wpk) +
                                ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + w.kb_begin) * (size_t)Cfg::FLT_STAGE;
             for (int i = 0; i < w.nkb; ++i, ++n) {
-                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
-                const uint32_t bar = smem_u32(&raw_full[stage]);
-                const uint32_t sbase = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES);
-                const uint32_t pix = sbase + Cfg::PIX_OFF;
-                const int kb = w.kb_begin + i;
-                // MODE 4 boxes are bx*by rows (<= 128): the rest of the tile keeps
-                // stale (finite) data whose output rows the epilogue discards.
-                const bool pre = n < npre;  // filter bytes already issued (and counted) for this stage
-                const uint32_t bytes = (MODE == 4   ? Cfg::BYTES - (uint32_t)(TM_M - a.bx * a.by) * 128u
-                                        : MODE == 6 ? Cfg::BYTES - (uint32_t)(TM_M - a.box_w * a.by) * 128u
-                                                    : Cfg::BYTES) -
-                                       (pre ? (uint32_t)Cfg::FLT_CTA : 0u);
-                mbar_arrive_expect_tx(bar, bytes);
-                if (n < 32) B2C_TRACE(a.trace, 176 + n);
-                if (MODE == 1) {
-                    tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
-                    tma_load_2d(sbase + Cfg::FLT_OFF, &tm_flt, bar, kb * TM_BK, w.n0);
-                } else if (MODE == 7) {  // V[z] rows and U[z] rows: (k, row, z)
-                    tma_load_3d(pix, &tm_pix, bar, kb * TM_BK, w.m0, w.b);
-                    tma_load_3d(sbase + Cfg::FLT_OFF, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
-                } else {
-                    if (MODE == 2) {
-                        tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
-                    } else if (MODE == 5) {  // (pixel run, channel block, image) straight from NCHW x
-                        tma_load_3d(pix, &tm_pix, bar, w.ox0, kb * TM_BK, w.b);
-                    } else if (MODE == 6) {  // (x, y, channel block, image) of NCHW x; x start rounded down to 16 B
-                        uint32_t tap, cb, ky, kx;
-                        a.fCB.divmod((uint32_t)kb, tap, cb);
-                        g.fR.divmod(tap, ky, kx);
-                        const int dx = w.ox0 + (int)kx - g.P;
-                        const int xs = ((dx >= 0 ? dx : dx - 3) / 4) * 4;  // floor to a multiple of 4 floats
-                        tma_load_4d(pix, &tm_pix, bar, xs, w.oy0 + (int)ky - g.P, (int)cb * TM_BK, w.b);
-                    } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
-                        uint32_t ky, kc;
-                        a.fCB.divmod((uint32_t)kb, ky, kc);
-                        tma_load_5d(pix, &tm_pix, bar, (int)kc * TM_BK, w.ox0, w.oy0, (int)ky, w.b);
-                    } else if (MODE == 0) {
-                        uint32_t tap, cb, ky, kx;
-                        a.fCB.divmod((uint32_t)kb, tap, cb);
-                        g.fR.divmod(tap, ky, kx);
-                        tma_load_im2col_4d(pix, &tm_pix, bar, (int)cb * TM_BK, pw, ph, pn, (uint16_t)kx, (uint16_t)ky);
-                    } else {  // MODE 3: 8 taps x 4 channels, one 16-byte-pixel box per tap
-#pragma unroll 1
-                        for (int j = 0; j < TM_TAPS; ++j) {
-                            const int tap = kb * TM_TAPS + j;
-                            uint32_t ky = 0, kx = 0;
-                            int c = 4;  // taps past R*R: channel 4 is out of bounds -> zeros
-                            if (tap < g.RR) {
-                                g.fR.divmod((uint32_t)tap, ky, kx);
-                                c = 0;
-                            }
-                            tma_load_im2col_4d(pix + (uint32_t)(j * Cfg::PIX_ROWS * 16), &tm_pix, bar, c, pw, ph, pn,
-                                               (uint16_t)kx, (uint16_t)ky);
-                        }
-                    }
-                    if (!pre) load_filters<Cfg::FLT_STAGE, CL>(sbase + Cfg::FLT_OFF, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
+                if (n >= npre) {  // (stages issued early were armed and loaded above)
+                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
+                    const uint32_t bar = smem_u32(&raw_full[stage]);
+                    const uint32_t dst = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::FLT_OFF;
+                    const int kb = w.kb_begin + i;
+                    mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
+                    if (MODE == 1)
+                        tma_load_2d(dst, &tm_flt, bar, kb * TM_BK, w.n0);
+                    else if (MODE == 7)  // U[z] rows: (k, row, z)
+                        tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
+                    else
+                        load_filters<Cfg::FLT_STAGE, CL>(dst, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
                 }
                 if (++stage == STAGES) {
                     stage = 0;

@@ -282,6 +282,32 @@ __global__ void __launch_bounds__(256) k_pack_filters_bf16(Geom g, const float* 
     }
 }
 
+// bf16 pack for MODE 8 (tm=5): per (filter tile, K block of 64 channels of one tap) the
+// SWIZZLE_128B K-major image the SS MMAs read: rows of 128 B (64 bf16), 16-byte chunk c
+// (elements 8c..8c+7) stored at chunk position c ^ (row % 8).
+__global__ void __launch_bounds__(256) k_pack_filters_bf16_sw128(Geom g, const float* __restrict__ w,
+                                                                 uint16_t* __restrict__ out, int rows, int kblocks,
+                                                                 FastDiv fCB, long long total) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)(i & 7);        // element within the stored 16-byte chunk
+        const int pc = (int)((i >> 3) & 7);  // stored chunk position in the 128-byte row
+        long long t = i >> 6;
+        const int r = (int)(t % rows);
+        t /= rows;
+        const int kb = (int)(t % kblocks);
+        const int tile = (int)(t / kblocks);
+        const int c = pc ^ (r & 7);  // logical chunk
+        const int oc = tile * rows + r;
+        uint32_t tap, cb, ky, kx;
+        fCB.divmod((uint32_t)kb, tap, cb);
+        g.fR.divmod(tap, ky, kx);
+        const int ic = (int)cb * 64 + 8 * c + e;
+        const float v = (oc < g.OC && ic < g.C) ? w[(long long)oc * g.K + ((long long)ic * g.R + ky) * g.R + kx] : 0.0f;
+        out[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    }
+}
+
 // e4m3 pack for the TMA kernel's fp8 mode: [filter tile][K block][16-element chunk 0..1][rows][16 x e4m3]
 // (UMMA no-swizzle K-major core matrices: 8 rows x 16 B contiguous), round to nearest even, saturating.
 __global__ void __launch_bounds__(256) k_pack_filters_e4m3(Geom g, const float* __restrict__ w,

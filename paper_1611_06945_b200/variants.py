@@ -272,7 +272,7 @@ class _UmmaFamily(Variant):
                 for split in (1, 2, 4, 8, 16, 32, 0):  # 0 = stream-K (TMA kernel)
                     if split > 1 and kblocks // split < 2:
                         continue
-                    for tma in ((1, 2, 3, 4) if split == 0 else (1, 2, 3, 4, 0)):
+                    for tma in ((1, 2, 3, 4, 5) if split == 0 else (1, 2, 3, 4, 5, 0)):  # 5: bf16 mode only
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
                         if tma and split and bn <= 64:  # two CTAs per SM
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))

@@ -39,7 +39,8 @@ def _params():
     return [TuneParams(bn=32, tma=1, prec=1), TuneParams(bn=64, split_k=2, tma=1, prec=1),
             TuneParams(bn=128, tma=2, prec=1), TuneParams(bn=192, split_k=0, tma=1, prec=1),
             TuneParams(bn=64, split_k=0, tma=2, prec=1), TuneParams(bn=64, tma=3, prec=1),
-            TuneParams(bn=128, split_k=2, tma=3, prec=1)]
+            TuneParams(bn=128, split_k=2, tma=3, prec=1), TuneParams(bn=64, tma=5, prec=1),
+            TuneParams(bn=128, split_k=2, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, prec=1)]
 
 
 def _graph(c, relu):
@@ -79,8 +80,12 @@ def test_bf16_full_size_signed(cuda, row, batch):
     x, f, b = conv_ref.conv_inputs(batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz, f"bf16:{row}", low=-1.0, high=1.0)
     want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
     bound = conv_ref.signed_bound(x, f, op.stride, op.pad)
-    for p in (TuneParams(bn=64, tma=1, prec=1), TuneParams(bn=128, split_k=0, tma=1, prec=1)):
+    for p in (TuneParams(bn=64, tma=1, prec=1), TuneParams(bn=128, split_k=0, tma=1, prec=1),
+              TuneParams(bn=128, split_k=0, tma=5, prec=1)):
         got = _run(g, x, f, b, p)
+        if got is None and p.tma == 5:  # the bf16-NHWC SS path needs in_chans % 8 == 0 (not first layers)
+            assert op.in_chans % 8 or op.in_chans <= 4
+            continue
         assert got is not None
         err = np.abs(got.astype(np.float64) - want.astype(np.float64))
         assert (err <= 8e-3 * bound + 1e-6).all(), (p.to_string(), float((err / (bound + 1e-30)).max()))
