@@ -123,7 +123,8 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
         if (t->variant != B2C_VAR_UMMA && t->variant != B2C_VAR_1X1) {
             why = "bf16 mode: tcgen05 conv_umma / conv_1x1 only"; return B2C_INAPPLICABLE;
         }
-        if (!t->tma || t->swap_ab || t->cluster >= 2 || t->stages == 2 || (t->tma == 2 && d->c <= 4)) {
+        const bool ss_pair = t->tma == 5 && t->cluster == 3;  // bf16 SS on 2-SM pairs
+        if (!t->tma || t->swap_ab || (t->cluster >= 2 && !ss_pair) || t->stages == 2 || (t->tma == 2 && d->c <= 4)) {
             why = "bf16 mode: TMA kernel (tma=1|2), swap_ab=0, single CTAs, not the 8-tap first-layer path";
             return B2C_INAPPLICABLE;
         }
@@ -225,9 +226,10 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->tma < 0 || t->tma > 5) { why = "tma must be 0..5"; return B2C_BAD_ARGS; }
     if (t->tma == 5) {  // bf16 mode: bf16 NHWC copy + SS MMAs (MODE 8)
         if (d->prec != B2C_PREC_BF16) { why = "tma=5 is the bf16 mode's NHWC-bf16 / SS-MMA path"; return B2C_INAPPLICABLE; }
-        if (t->variant == B2C_VAR_FC || t->swap_ab || t->cluster >= 2 || t->stages == 2) {
-            why = "tma=5: a conv variant, pixels on M, single CTAs, 1 CTA/SM"; return B2C_INAPPLICABLE;
+        if (t->variant == B2C_VAR_FC || t->swap_ab || t->cluster == 2 || t->cluster == 4 || t->stages == 2) {
+            why = "tma=5: a conv variant, pixels on M, single CTAs or 2-SM pairs, 1 CTA/SM"; return B2C_INAPPLICABLE;
         }
+        if (t->cluster == 3 && t->tile_n == 64) { why = "tma=5 pairs: tile_n 128 | 192"; return B2C_INAPPLICABLE; }
         if (d->c % 8 || d->c <= 4) { why = "tma=5 needs in_chans % 8 == 0 (16-byte bf16 NHWC pixels)"; return B2C_INAPPLICABLE; }
         if (t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) { why = "tma=5: tile_n in {64, 128, 192}"; return B2C_INAPPLICABLE; }
         if (t->split_k < 0) { why = "split_k must be >= 0"; return B2C_BAD_ARGS; }
@@ -261,7 +263,9 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
         }
         if (t->tma == 2) { why = "2-SM UMMA pairs: not with tma=2 (2-D tiles / 8-tap first-layer boxes)"; return B2C_INAPPLICABLE; }
         if (t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) { why = "2-SM UMMA pairs: tile_n in {64, 128, 192}"; return B2C_INAPPLICABLE; }
-        if (d->prec != B2C_PREC_FP32) { why = "2-SM UMMA pairs: fp32-exact mode only"; return B2C_INAPPLICABLE; }
+        if (d->prec != B2C_PREC_FP32 && !(d->prec == B2C_PREC_BF16 && t->tma == 5)) {
+            why = "2-SM UMMA pairs: fp32-exact mode, or the bf16 SS path (tma=5)"; return B2C_INAPPLICABLE;
+        }
     }
     if (t->tma == 2 && !(d->r == 1 && d->stride == 1 && d->pad == 0) && t->variant != B2C_VAR_FC && d->c > 4) {
         why = "tma=2 (2-D tiled pixels) needs a 1x1, stride 1, pad 0 conv"; return B2C_INAPPLICABLE;
@@ -748,7 +752,10 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
             : mode == 4 ? tconv_pick_bf16<4>(t->tile_n) : mode == 5 ? tconv_pick_bf16<5>(t->tile_n)
             : mode == 6 ? tconv_pick_bf16<6>(t->tile_n)
-            : mode == 8 ? tconv_pick_bf16<8>(t->tile_n)
+            : mode == 8 ? (cl == 3 ? (t->tile_n == 128 ? tconv_entry<128, false, 8, 1, 3, 1>()
+                                      : t->tile_n == 192 ? tconv_entry<192, false, 8, 1, 3, 1>()
+                                                         : TconvEntry{nullptr, 0, 0})
+                                   : tconv_pick_bf16<8>(t->tile_n))
             : TconvEntry{nullptr, 0, 0};
     else if (d->prec == B2C_PREC_FP8)
         e = mode == 0 ? tconv_pick_fp8<0>(t->tile_n) : mode == 4 ? tconv_pick_fp8<4>(t->tile_n)

@@ -140,6 +140,16 @@ __device__ __forceinline__ void mma_tf32_ts_pair(uint32_t tmem_d, uint32_t tmem_
         "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// D[tmem] (+)= A[smem] * B[smem]^T over the pair, kind::f16 bf16 (M = 256, K = 16).
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // Relaxed arrive on the mbarrier at shared offset `bar` of cluster CTA `rank`: orders nothing
 // but itself (a drain warp's TMEM reads are complete at tcgen05.wait::ld; a release here would
 // also wait for the previous unit's global stores to be performed at cluster scope).

@@ -92,10 +92,10 @@ constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
 // filter tile (B rows) and its own 128 accumulator rows.
 template <int BN, bool SWAP, int MODE, int OCC = 1, int CL = 1, int PREC = 0>
 struct TmaCfg {
-    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && MODE != 7 && CL == 1), "bf16 / fp8: pixels on M, packed filters");
+    static_assert(PREC == 0 || (!SWAP && MODE != 1 && MODE != 3 && MODE != 7 && (CL == 1 || MODE == 8)), "bf16 / fp8: pixels on M, packed filters");
     static constexpr bool RAW_B = MODE == 1 || MODE == 7;  // both operands raw [rows][K] matrices by TMA (no pack)
     static constexpr bool SS = MODE == 8;  // bf16 NHWC copy: A and B straight from shared memory, no split pass
-    static_assert(!SS || (PREC == 1 && !SWAP && CL == 1 && OCC == 1), "MODE 8: bf16, pixels on M, single CTAs");
+    static_assert(!SS || (PREC == 1 && !SWAP && (CL == 1 || CL == 3) && OCC == 1), "MODE 8: bf16, pixels on M, single CTAs or 2-SM pairs");
     static_assert((MODE != 5 && MODE != 6) || CL != 2, "MODE 5/6: no multicast pairs");
     static_assert(CL == 1 || CL == 4 || ((CL == 2 || CL == 3) && !SWAP && !RAW_B && OCC == 1), "pairs share B = packed filters");
     static_assert(CL != 4 || OCC == 1, "cluster split-K: one CTA per SM (the staging tile)");
@@ -125,7 +125,7 @@ struct TmaCfg {
     static constexpr bool A_PRESPLIT = false;
     static constexpr bool B_SPLIT = SWAP || RAW_B;  // B raw from TMA: lo computed into smem
     static constexpr int A_SMEM = (A_PRESPLIT ? 2 : 1) * TM_M * 128;
-    static constexpr int B_BYTES = SS ? BN * 128 : PREC == 1 ? BN * 64 : PREC == 2 ? BN * 32
+    static constexpr int B_BYTES = SS ? (PAIR ? BN / 2 : BN) * 128 : PREC == 1 ? BN * 64 : PREC == 2 ? BN * 32
                                                              : (PAIR ? 1 : 2) * BN * 128;  // bf16 SW128 64-K | bf16 | e4m3 | raw + lo (a pair: half the rows each)
     static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int PIX_OFF = SWAP ? A_SMEM : 0;
@@ -133,7 +133,7 @@ struct TmaCfg {
     static constexpr int FLT_STAGE = SS ? FLT_ROWS * 128 : PREC == 1 ? FLT_ROWS * 64 : PREC == 2 ? FLT_ROWS * 32
                                                                  : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
     static constexpr int FLT_HALF = FLT_ROWS / 2 * 128;   // 2-SM pair: one CTA's rows of one (raw | lo) image
-    static constexpr int FLT_CTA = PAIR ? 2 * FLT_HALF : FLT_STAGE;  // filter bytes landing in one CTA per K block
+    static constexpr int FLT_CTA = PAIR ? (SS ? FLT_HALF : 2 * FLT_HALF) : FLT_STAGE;  // filter bytes landing in one CTA per K block
     static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
     // OCC CTAs per SM share its 228 KB of shared memory (1 KB per CTA is the driver's) and 512 TMEM columns
     static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024 - STG_BYTES;
@@ -151,7 +151,8 @@ struct TmaCfg {
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (RAW_B ? FLT_ROWS * 128 : FLT_CTA);
     static constexpr uint32_t FLT_BYTES = RAW_B ? FLT_ROWS * 128 : FLT_CTA;  // the filter warp's bytes per stage
     // barrier arrival counts (a pair's leader counts its peer's split / drain warps too)
-    static constexpr int SPLIT_ARRIVALS = PAIR ? 2 * (TM_SPLIT_THREADS / 32) : TM_SPLIT_THREADS;
+    // (SS pairs: one forwarding lane per CTA reports its stage's TMA bytes to the leader)
+    static constexpr int SPLIT_ARRIVALS = PAIR ? (SS ? 2 : 2 * (TM_SPLIT_THREADS / 32)) : TM_SPLIT_THREADS;
     static constexpr int DRAIN_ARRIVALS = PAIR ? 2 * (DRAIN_THREADS / 32) : DRAIN_THREADS;
     static_assert(MODE != 4 || !SWAP, "MODE 4 tiles are pixel blocks on M");
     static_assert((MODE != 5 && MODE != 6) || !SWAP, "MODE 5/6 tiles are pixel blocks on M (split warps transpose them)");
@@ -462,9 +463,12 @@ __device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
 
 // One K block of packed filters into a stage: one bulk copy, or, in a 2-CTA
 // pair, each CTA fetches half (raw | lo) and multicasts it to both.
-template <int BYTES, int CL>
+template <int BYTES, int CL, bool ONE_IMAGE = false>
 __device__ __forceinline__ void load_filters(uint32_t dst, const char* src, uint32_t bar, int rank) {
-    if (CL == 3) {  // 2-SM pair: this CTA's half of the rows of the raw image and of the lo image
+    if (CL == 3 && ONE_IMAGE) {  // 2-SM pair, one image per K block (bf16 SS): this CTA's half of its rows
+        constexpr uint32_t H = BYTES / 2;
+        bulk_g2s(dst, src + (size_t)rank * H, H, bar);
+    } else if (CL == 3) {  // 2-SM pair: this CTA's half of the rows of the raw image and of the lo image
         constexpr uint32_t H = BYTES / 4;
         bulk_g2s(dst, src + (size_t)rank * H, H, bar);
         bulk_g2s(dst + H, src + BYTES / 2 + (size_t)rank * H, H, bar);
@@ -824,6 +828,23 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
 
     if (warp < 4) {
         // ------------------------------------------------------------ split: A -> TMEM (raw | lo), B lo -> smem
+        if constexpr (Cfg::SS && Cfg::PAIR) {  // SS pair: forward this CTA's stage-full to the leader's MMA warp
+            if (warp == 0 && lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+                for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
+                    for (int i = 0; i < w.nkb; ++i) {
+                        mbar_wait(smem_u32(&raw_full[stage]), phase);
+                        mbar_arrive_cluster_relaxed(smem_u32(&split_full[stage]), 0);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+                }
+            }
+        }
         if constexpr (!Cfg::SS) {  // MODE 8: the MMAs read both operands from shared memory (no split)
         int stage = 0, n = 0;
         uint32_t phase = 0;
@@ -944,7 +965,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 // raw_full, so it also covers the TMA / bulk bytes (a pair: both CTAs').
                 if (Cfg::PAIR)
                     mbar_wait_cluster(smem_u32(&split_full[stage]), phase);
-                else if (Cfg::SS)  // no split pass: wait for the TMA / bulk bytes themselves
+                else if (Cfg::SS)  // no split pass: wait for the TMA / bulk bytes themselves (a pair: forwarded)
                     mbar_wait(smem_u32(&raw_full[stage]), phase);
                 else
                     mbar_wait(smem_u32(&split_full[stage]), phase);
@@ -961,8 +982,12 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
 #pragma unroll
                         for (int s = 0; s < 4; ++s) {
                             if (s >= nsteps) break;  // all-zero channel tail
-                            mma_bf16(d, umma_desc_sw128(a_s + s * 32), umma_desc_sw128(b_raw + s * 32), idesc,
-                                     (first && s == 0) ? 0u : 1u);
+                            if constexpr (Cfg::PAIR)
+                                mma_bf16_pair(d, umma_desc_sw128(a_s + s * 32), umma_desc_sw128(b_raw + s * 32), idesc,
+                                              (first && s == 0) ? 0u : 1u);
+                            else
+                                mma_bf16(d, umma_desc_sw128(a_s + s * 32), umma_desc_sw128(b_raw + s * 32), idesc,
+                                         (first && s == 0) ? 0u : 1u);
                         }
                     } else if constexpr (PREC == 2) {  // e4m3: one K=32 MMA per K block ([2 chunks][rows][16 B])
                         mma_e4m3_ts(d, a_hi, umma_desc(b_raw, BN * 16, 128), idesc, first ? 0u : 1u);
@@ -1064,7 +1089,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     else if (MODE == 7)
                         tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
                     else
-                        load_filters<Cfg::FLT_STAGE, CL>(
+                        load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(
                             dst, reinterpret_cast<const char*>(a.wpk) +
                                      ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + kb) * (size_t)Cfg::FLT_STAGE, bar, rank);
                 }
@@ -1127,7 +1152,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 for (int i = 0; i < npre; ++i) {  // fresh stages: no empty wait
                     const uint32_t bar = smem_u32(&raw_full[i]);
                     mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
-                    load_filters<Cfg::FLT_STAGE, CL>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
+                    load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
                                                     wsrc0 + (size_t)i * Cfg::FLT_STAGE, bar, rank);
                 }
             }
@@ -1151,7 +1176,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     else if (MODE == 7)  // U[z] rows: (k, row, z)
                         tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
                     else
-                        load_filters<Cfg::FLT_STAGE, CL>(dst, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
+                        load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(dst, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
                 }
                 if (++stage == STAGES) {
                     stage = 0;

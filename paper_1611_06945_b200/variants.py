@@ -278,7 +278,7 @@ class _UmmaFamily(Variant):
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))
                         if tma in (1, 2) and split and bn >= 64 and not swap:  # CTA pairs multicasting filters
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
-                        if tma in (1, 3, 4) and bn in (64, 128, 192) and not swap:  # 2-SM UMMA pairs (M = 256)
+                        if (tma in (1, 3, 4) and bn in (64, 128, 192) or tma == 5 and bn in (128, 192)) and not swap:  # 2-SM UMMA pairs (M = 256)
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=3))
                         if 2 <= split <= 8 and tma in (1, 3, 4) and (bn in (32, 64) and not swap or bn == 32 and swap):
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=4))  # split-K cluster

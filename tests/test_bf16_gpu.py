@@ -40,7 +40,9 @@ def _params():
             TuneParams(bn=128, tma=2, prec=1), TuneParams(bn=192, split_k=0, tma=1, prec=1),
             TuneParams(bn=64, split_k=0, tma=2, prec=1), TuneParams(bn=64, tma=3, prec=1),
             TuneParams(bn=128, split_k=2, tma=3, prec=1), TuneParams(bn=64, tma=5, prec=1),
-            TuneParams(bn=128, split_k=2, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, prec=1)]
+            TuneParams(bn=128, split_k=2, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, prec=1),
+            TuneParams(bn=128, tma=5, cl=3, prec=1), TuneParams(bn=192, split_k=2, tma=5, cl=3, prec=1),
+            TuneParams(bn=128, split_k=0, tma=5, cl=3, prec=1)]
 
 
 def _graph(c, relu):
@@ -81,7 +83,7 @@ def test_bf16_full_size_signed(cuda, row, batch):
     want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
     bound = conv_ref.signed_bound(x, f, op.stride, op.pad)
     for p in (TuneParams(bn=64, tma=1, prec=1), TuneParams(bn=128, split_k=0, tma=1, prec=1),
-              TuneParams(bn=128, split_k=0, tma=5, prec=1)):
+              TuneParams(bn=128, split_k=0, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, cl=3, prec=1)):
         got = _run(g, x, f, b, p)
         if got is None and p.tma == 5:  # the bf16-NHWC SS path needs in_chans % 8 == 0 (not first layers)
             assert op.in_chans % 8 or op.in_chans <= 4
