@@ -262,7 +262,8 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             return B2C_INAPPLICABLE;
         }
         if (t->tma == 2) { why = "2-SM UMMA pairs: not with tma=2 (2-D tiles / 8-tap first-layer boxes)"; return B2C_INAPPLICABLE; }
-        if (t->tile_n != 64 && t->tile_n != 128 && t->tile_n != 192) { why = "2-SM UMMA pairs: tile_n in {64, 128, 192}"; return B2C_INAPPLICABLE; }
+        if (t->tile_n != 64 && t->tile_n != 96 && t->tile_n != 128 && t->tile_n != 192) { why = "2-SM UMMA pairs: tile_n in {64, 96, 128, 192}"; return B2C_INAPPLICABLE; }
+        if (t->tile_n == 96 && t->tma == 5) { why = "tma=5 pairs: tile_n 128 | 192"; return B2C_INAPPLICABLE; }
         if (d->prec != B2C_PREC_FP32 && !(d->prec == B2C_PREC_BF16 && t->tma == 5)) {
             why = "2-SM UMMA pairs: fp32-exact mode, or the bf16 SS path (tma=5)"; return B2C_INAPPLICABLE;
         }
@@ -687,6 +688,7 @@ TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
         if constexpr (!SWAP && MODE != 1 && MODE != 2 && MODE != 3) {
             switch (bn) {
                 case 64: return tconv_entry<64, false, MODE, 1, 3>();
+                case 96: return tconv_entry<96, false, MODE, 1, 3>();
                 case 128: return tconv_entry<128, false, MODE, 1, 3>();
                 case 192: return tconv_entry<192, false, MODE, 1, 3>();
             }

@@ -201,9 +201,10 @@ def candidates(node: OpNode, edges, space: TuneSpace | None = None, prec: int = 
     out = []
     for v in variants_for_kind(node.kind):
         plist = space.per_variant.get(v.name)
-        plist = v.space(node, edges) if plist is None else list(plist)
-        if prec:
-            plist = with_prec(plist, prec)
+        if plist is None:
+            plist = v.space(node, edges, prec)  # the variant's own space, built and filtered in mode `prec`
+        else:
+            plist = with_prec(list(plist), prec) if prec else list(plist)
         out.extend((v, p) for p in v.tune_candidates(node, edges, plist))
     return out
 

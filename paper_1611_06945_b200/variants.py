@@ -197,9 +197,15 @@ class Variant:
     def default_params(self, node: OpNode, edges) -> TuneParams:
         return DEFAULT_TUNE
 
-    def space(self, node: OpNode, edges) -> list:
-        """This variant's own candidate list for the on-device sweep."""
-        return [self.default_params(node, edges)]
+    def space(self, node: OpNode, edges, prec: int = 0) -> list:
+        """This variant's own candidate list for the on-device sweep, in precision mode ``prec``
+        (candidates are filtered by applicability in that mode)."""
+        p = self.default_params(node, edges)
+        if prec:
+            from dataclasses import replace
+
+            p = replace(p, prec=prec)
+        return [p] if self.applies(node, edges, p) is None else []
 
     def tune_candidates(self, node: OpNode, edges, candidates):
         return [p for p in candidates if self.applies(node, edges, p) is None]
@@ -218,7 +224,9 @@ class ConvSimple(Variant):
 class ConvTiled(Variant):
     name, rank, vid = "conv_tiled", 1, backend.VAR_TILED
 
-    def space(self, node, edges):
+    def space(self, node, edges, prec: int = 0):
+        if prec:
+            return []  # FFMA kernels are fp32-exact only
         out = []
         for mnt in ((4, 4), (8, 8), (8, 4), (4, 8)):
             for mnb in ((16, 16), (32, 8), (8, 32), (16, 8)):
@@ -260,7 +268,9 @@ class _UmmaFamily(Variant):
             return p
         return TuneParams(bn=bn, split_k=split, swap_ab=swap)
 
-    def space(self, node, edges):
+    def space(self, node, edges, prec: int = 0):
+        from dataclasses import replace
+
         s = conv_shape(node, edges)
         kblocks = _ceil(s.k, 32)
         out = []
@@ -278,10 +288,12 @@ class _UmmaFamily(Variant):
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))
                         if tma in (1, 2) and split and bn >= 64 and not swap:  # CTA pairs multicasting filters
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
-                        if (tma in (1, 3, 4) and bn in (64, 128, 192) or tma == 5 and bn in (128, 192)) and not swap:  # 2-SM UMMA pairs (M = 256)
+                        if (tma in (1, 3, 4) and bn in (64, 96, 128, 192) or tma == 5 and bn in (128, 192)) and not swap:  # 2-SM UMMA pairs (M = 256)
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=3))
                         if 2 <= split <= 8 and tma in (1, 3, 4) and (bn in (32, 64) and not swap or bn == 32 and swap):
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=4))  # split-K cluster
+        if prec:
+            out = [replace(p, prec=prec) for p in out]
         return [p for p in out if self.applies(node, edges, p) is None]
 
 
@@ -319,7 +331,9 @@ class ConvWino(Variant):
     def default_params(self, node, edges):
         return TuneParams(bn=128, split_k=1, tma=1)
 
-    def space(self, node, edges):
+    def space(self, node, edges, prec: int = 0):
+        if prec:
+            return []  # fp32-exact only
         out = [TuneParams(bn=bn, split_k=sk, swap_ab=sw, tma=1) for sw in (False, True) for bn in (64, 128, 192)
                for sk in (1, 2, 4, 0)]
         return [p for p in out if self.applies(node, edges, p) is None]
@@ -337,7 +351,9 @@ class ConvFCStream(Variant):
     def default_params(self, node, edges):
         return TuneParams(mnt=(1, 4), mnb=(8, 1), kb=1, vw=1)
 
-    def space(self, node, edges):
+    def space(self, node, edges, prec: int = 0):
+        if prec:
+            return []  # fp32-exact only
         out = [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=1, vw=1) for wp in (2, 4, 8) for r in (2, 4, 8)]
         out += [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=2, vw=1) for wp in (4, 8) for r in (1, 2, 4)]
         return [p for p in out if self.applies(node, edges, p) is None]
@@ -447,7 +463,7 @@ def select_variant(node: OpNode, edges, db=None, prec: int | None = None):
             return v, params
     if prec:  # no heuristic tile applies in this mode: the first applicable candidate of the mode
         for v in variants_for_kind(node.kind):
-            for params in with_prec(v.space(node, edges) if hasattr(v, "space") else [], prec):
+            for params in (v.space(node, edges, prec) if hasattr(v, "space") else []):
                 if v.applies(node, edges, params) is None:
                     return v, params
     raise Inapplicable(f"no variant for node '{node.name}' of kind {node.kind}" +

@@ -66,7 +66,7 @@ def _variant_params(g):
                     TuneParams(bn=64, tma=4, occ=2), TuneParams(bn=64, tma=1, cl=3),
                     TuneParams(bn=128, split_k=2, tma=1, cl=3), TuneParams(bn=192, tma=1, cl=3),
                     TuneParams(bn=128, tma=4, cl=3), TuneParams(bn=64, split_k=2, tma=3, cl=3),
-                    TuneParams(bn=128, tma=3, cl=3), TuneParams(bn=128, split_k=0, tma=1, cl=3),
+                    TuneParams(bn=128, tma=3, cl=3), TuneParams(bn=128, split_k=0, tma=1, cl=3), TuneParams(bn=96, tma=1, cl=3),
                     TuneParams(bn=64, split_k=0, tma=4, cl=3), TuneParams(bn=32, split_k=2, tma=1, cl=4),
                     TuneParams(bn=64, split_k=4, tma=1, cl=4), TuneParams(bn=32, split_k=3, tma=3, cl=4),
                     TuneParams(bn=64, split_k=2, tma=4, cl=4), TuneParams(bn=32, swap_ab=True, split_k=4, tma=1, cl=4)):
