@@ -114,7 +114,11 @@ typedef struct b2c_tune {
                     3 = 1x1 / stride 1 / pad 0 convs read straight from NCHW x (3-D TMA box
                         [32 ch][128 px] per K block; h*w*4 bytes a multiple of 16; no re-layout launch);
                     4 = k x k stride-1 convs read straight from NCHW x (4-D TMA box of whole output
-                        rows, x start rounded down to 16 bytes; input width a multiple of 4) */
+                        rows, x start rounded down to 16 bytes; input width a multiple of 4);
+                    5 = bf16 mode: a bf16 NHWC copy of x and SS MMAs (64-channel K blocks, no split pass);
+                    6 = first layers (C <= 4, stride 2..4): space-to-depth -- the conv runs as an
+                        R' x R' stride-1 conv (R' = ceil(R/S)) over a C*S*S-channel copy of x with
+                        re-arranged filters, on the im2col path of tma=1 */
     int32_t cluster; /* TMA kernel: 2 = CTA pairs (thread-block clusters) take neighbouring pixel tiles of the
                         same filter tile and multicast each filter stage to both (half the filter L2 traffic);
                         3 = 2-SM UMMA pairs: the same two pixel tiles as ONE tcgen05.mma.cta_group::2 of

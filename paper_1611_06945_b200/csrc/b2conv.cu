@@ -113,6 +113,43 @@ int is_pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1
 
 // ----------------------------------------------------------------------------- applicability
 
+// ----------------------------------------------------------------------------- first-layer space-to-depth (tma = 6)
+// An R x R stride-S conv with C <= 4 channels is rewritten as an R' x R' stride-1 conv
+// (R' = ceil(R/S)) over a space-to-depth copy of x with C*S*S channels (k_s2d_nhwc) and
+// re-arranged filters (k_s2d_filters), then run on the ordinary im2col TMA path (tm=1):
+// AlexNet / NiN conv1 (11x11 s4, C=3) become 3x3 convs over 48 channels -- 18 K blocks
+// per 128-pixel tile instead of 22 per 110-pixel tile with the x-window packing.
+struct S2d {
+    b2c_conv_desc d2;
+    b2c_tune t2;
+    int S;
+};
+
+bool s2d_of(const b2c_conv_desc* d, const b2c_tune* t, S2d& o) {
+    if (!d || !t || t->tma != 6) return false;
+    const int S = d->stride, R2 = (d->r + S - 1) / S;
+    const int Hs = std::max((d->h + 2 * d->pad + S - 1) / S, d->oh + R2 - 1);
+    const int Ws = std::max((d->w + 2 * d->pad + S - 1) / S, d->ow + R2 - 1);
+    o.S = S;
+    o.d2 = b2c_conv_desc{d->n, d->c * S * S, Hs, Ws, d->k, R2, 1, 0, d->oh, d->ow, d->act, d->prec};
+    o.t2 = *t;
+    o.t2.tma = 1;
+    return true;
+}
+
+int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why);
+
+int applies_s2d(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
+    if (t->variant != B2C_VAR_UMMA || d->prec != B2C_PREC_FP32) { why = "tma=6 (first-layer space-to-depth): conv_umma, fp32-exact"; return B2C_INAPPLICABLE; }
+    if (d->c > 4 || (d->stride != 2 && d->stride != 4) || d->r <= d->stride || (d->c * d->stride * d->stride) % 4 ||
+        d->c * d->stride * d->stride <= 4) {
+        why = "tma=6: first layers (C <= 4) with stride 2 or 4 < ksz and C*stride^2 a multiple of 4 above 4"; return B2C_INAPPLICABLE;
+    }
+    S2d o;
+    s2d_of(d, t, o);
+    return applies_impl(&o.d2, &o.t2, why);
+}
+
 int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     int rc = check_desc(d);
     if (rc) { why = g_last_error; return rc; }
@@ -223,7 +260,8 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
     if (t->split_k == 0 && (t->cluster == 2 || t->stages == 2)) { why = "stream-K: single CTAs or 2-SM pairs"; return B2C_INAPPLICABLE; }
     if (t->swap_ab != 0 && t->swap_ab != 1) { why = "swap_ab must be 0 or 1"; return B2C_BAD_ARGS; }
     if (t->drain < 0 || t->drain > 64) { why = "drain must be in [0, 64]"; return B2C_BAD_ARGS; }
-    if (t->tma < 0 || t->tma > 5) { why = "tma must be 0..5"; return B2C_BAD_ARGS; }
+    if (t->tma < 0 || t->tma > 6) { why = "tma must be 0..6"; return B2C_BAD_ARGS; }
+    if (t->tma == 6) return applies_s2d(d, t, why);
     if (t->tma == 5) {  // bf16 mode: bf16 NHWC copy + SS MMAs (MODE 8)
         if (d->prec != B2C_PREC_BF16) { why = "tma=5 is the bf16 mode's NHWC-bf16 / SS-MMA path"; return B2C_INAPPLICABLE; }
         if (t->variant == B2C_VAR_FC || t->swap_ab || t->cluster == 2 || t->cluster == 4 || t->stages == 2) {
@@ -420,6 +458,17 @@ bool is_umma(int variant) { return variant == B2C_VAR_UMMA || variant == B2C_VAR
 
 int pack_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* ws, size_t ws_bytes,
               cudaStream_t st) {
+    S2d o;
+    if (s2d_of(d, t, o)) {  // re-arrange the filters past the rewritten conv's workspace, then pack those
+        const size_t base = umma_plan(&o.d2, &o.t2).ws_bytes;
+        const size_t w2b = (size_t)o.d2.k * o.d2.c * o.d2.r * o.d2.r * sizeof(float);
+        if (!ws || ws_bytes < base + align256(w2b)) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+        float* w2 = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + base);
+        const long long total = (long long)(w2b / sizeof(float));
+        k_s2d_filters<<<(unsigned)std::min<long long>((total + 255) / 256, 148LL * 16), 256, 0, st>>>(
+            w, w2, d->k, d->c, d->r, o.S, o.d2.r);
+        return pack_impl(&o.d2, &o.t2, w2, ws, base, st);
+    }
     const UmmaPlan p = umma_plan(d, t);
     if (p.wpk_bytes == 0) return B2C_OK;  // TMA fc path reads raw filters
     if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
@@ -742,7 +791,8 @@ int num_sms() {
 }
 
 int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const Geom& g, const float* x,
-            const float* w, const float* bias, float* y, void* ws, cudaStream_t st) {
+            const float* w, const float* bias, float* y, void* ws, cudaStream_t st,
+            const b2c_conv_desc* s2d_src = nullptr) {  // s2d_src: the original first-layer conv (tma = 6)
     int rc = load_tma_encoders();
     if (rc) return rc;
     const bool plain_1x1 = d->r == 1 && d->stride == 1 && d->pad == 0;
@@ -819,13 +869,17 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
         float* xh = reinterpret_cast<float*>(wsb + p.nhwc_off);
         const int HW = d->h * d->w;
         const int cp = mode == 3 ? 4 : d->c;
-        if (!separate && mode != 3) relayout = 1;
+        if (!separate && mode != 3 && !s2d_src) relayout = 1;
         else if (!(g_trace_on & 16)) {  // debug bit 4: reuse the NHWC copy already in the workspace
             cudaError_t le;
             if (mode == 3) {
                 const long long total = (long long)d->n * HW;
                 le = launch_pdl(k_to_nhwc4_pad, dim3(d->n * d->h), dim3(d->w > 128 ? 256 : 128), 0, st, 1, x, reinterpret_cast<float4*>(xh),
                                 (int)d->c, (int)d->h, (int)d->w, (int)d->h, (int)d->w, 0, total);
+            } else if (s2d_src) {  // x -> its space-to-depth NHWC copy (d is the rewritten conv)
+                auto ks = s2d_src->stride == 4 ? k_s2d_nhwc<4> : k_s2d_nhwc<2>;  // S*S % 4 == 0: float4 stores
+                le = launch_pdl(ks, dim3(d->n * d->h), dim3(256), 0, st, 1, x, xh, (int)s2d_src->c, (int)s2d_src->h,
+                                (int)s2d_src->w, (int)s2d_src->pad, (int)d->h, (int)d->w);
             } else {
                 dim3 tgrid((HW + 31) / 32, (cp + 31) / 32, d->n);
                 le = launch_pdl(k_nchw_to_nhwc, tgrid, dim3(256), 0, st, 1, x, xh, (int)d->c, cp, HW);
@@ -1072,6 +1126,21 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
     int rc = applies_impl(d, t, why);
     if (rc) return fail(rc, why);
     if (!x || !w || !bias || !y) return fail(B2C_BAD_ARGS, "null tensor pointer");
+    {
+        S2d o;
+        if (s2d_of(d, t, o)) {  // first-layer space-to-depth: the rewritten 3x3-class conv on the TMA path
+            if (!t->prepared) {
+                rc = pack_impl(d, t, w, ws, ws_bytes, st);
+                if (rc) return rc;
+            }
+            const UmmaPlan p2 = umma_plan(&o.d2, &o.t2);
+            if (!ws || ws_bytes < p2.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
+            rc = tma_fwd(&o.d2, &o.t2, p2, make_geom(&o.d2), x, w, bias, y, ws, st, d);
+            if (rc) return rc;
+            cudaError_t le = cudaGetLastError();
+            return le == cudaSuccess ? B2C_OK : cuda_fail(le, "kernel launch");
+        }
+    }
     const Geom g = make_geom(d);
     switch (t->variant) {
         case B2C_VAR_SIMPLE: {
@@ -1238,6 +1307,9 @@ size_t b2c_conv_workspace(const b2c_conv_desc* d, const b2c_tune* t) {
     std::string why;
     if (applies_impl(d, t, why)) return 0;
     if (t->variant == B2C_VAR_WINO) return wino_plan(d, t).ws_bytes;
+    S2d o;
+    if (s2d_of(d, t, o))  // the rewritten conv's workspace + the re-arranged filters (used while packing)
+        return umma_plan(&o.d2, &o.t2).ws_bytes + align256((size_t)o.d2.k * o.d2.c * o.d2.r * o.d2.r * sizeof(float));
     if (!is_umma(t->variant)) return 0;
     return umma_plan(d, t).ws_bytes;
 }
@@ -1339,7 +1411,9 @@ int b2c_conv_fwd_host(const b2c_conv_desc* d, const b2c_tune* t, const float* hx
         B2C_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ws) + wp.sems_off, 0, wp.ws_bytes - wp.sems_off, st));
     }
     if (wsb && is_umma(t->variant)) {
-        const UmmaPlan up = umma_plan(d, t);
+        S2d o;
+        const bool s2d = s2d_of(d, t, o);
+        const UmmaPlan up = s2d ? umma_plan(&o.d2, &o.t2) : umma_plan(d, t);
         if (up.nhwc_off > up.sems_off)
             B2C_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ws) + up.sems_off, 0, up.nhwc_off - up.sems_off, st));
         if (up.ws_bytes > up.gbar_off)
@@ -1371,6 +1445,7 @@ int b2c_conv_launches(const b2c_conv_desc* d, const b2c_tune* t) {
     (void)d;
     if (!t) return 0;
     if (t->variant == B2C_VAR_WINO) return 3 + (t->prepared ? 0 : 1);  // input transform, GEMM, output transform
+    if (t->tma == 6) return 2 + (t->prepared ? 0 : 2);  // s2d copy + conv (+ filter re-arrangement + pack)
     const int pack = (is_umma(t->variant) && !t->prepared && !(t->tma && t->variant == B2C_VAR_FC)) ? 1 : 0;
     const bool sep = std::getenv("B2C_FUSED_NHWC") == nullptr || (t->tma == 2 && d && d->c <= 4);
     const int nhwc = (is_umma(t->variant) && t->tma && t->tma != 3 && t->tma != 4 && t->variant != B2C_VAR_FC && sep) ? 1 : 0;
@@ -1397,6 +1472,8 @@ int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t) {
         case B2C_VAR_FC_STREAM:
             return t->kb == 2 ? (g.OC + t->mnb0 * t->mnt1 - 1) / (t->mnb0 * t->mnt1) : (g.OC + t->mnt1 - 1) / t->mnt1;
         default: {
+            S2d o;
+            if (s2d_of(d, t, o)) return b2c_conv_grid(&o.d2, &o.t2);
             const UmmaPlan p = umma_plan(d, t);
             if (!t->tma) return p.grid_x * p.grid_y * p.split;
             const int occ = t->stages == 2 ? 2 : 1, cl = (t->cluster == 2 || t->cluster == 3) ? 2 : 1;

@@ -355,6 +355,57 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc_bf16(const float* __restri
     }
 }
 
+// First layers, space-to-depth (tm=6): x [N][C][H][W] -> xs [N][H'][W'][C*S*S] with
+// xs[n][Y][X][(c*S + dy)*S + dx] = x[n][c][S*Y + dy - P][S*X + dx - P] (0 outside): an
+// R x R stride-S conv over x is an R' x R' stride-1 conv over xs (R' = ceil(R/S)) with
+// C*S*S channels.  One block per (image, output row Y); the stores run along (X, c').
+template <int S>
+__global__ void __launch_bounds__(256) k_s2d_nhwc(const float* __restrict__ x, float* __restrict__ xs, int C, int H,
+                                                  int W, int P, int Hs, int Ws) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int n = blockIdx.x / Hs, Y = blockIdx.x - n * Hs;
+    const int C2 = C * S * S;
+    float* dst = xs + ((size_t)n * Hs + Y) * Ws * C2;
+    // one thread per (output pixel X, input channel c): S*S consecutive channels of xs, float4 stores
+    for (int i = threadIdx.x; i < Ws * C; i += blockDim.x) {
+        const int X = i / C, c = i - X * C;
+        const float* src = x + ((size_t)n * C + c) * H * W;
+        float v[S * S];
+#pragma unroll
+        for (int dy = 0; dy < S; ++dy) {
+            const int iy = S * Y + dy - P;
+#pragma unroll
+            for (int dx = 0; dx < S; ++dx) {
+                const int ix = S * X + dx - P;
+                v[dy * S + dx] = ((unsigned)iy < (unsigned)H && (unsigned)ix < (unsigned)W) ? __ldg(src + (size_t)iy * W + ix) : 0.0f;
+            }
+        }
+        float4* o = reinterpret_cast<float4*>(dst + (size_t)X * C2 + c * S * S);
+#pragma unroll
+        for (int q = 0; q < S * S / 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+}
+
+// The matching filter transform (once per filter tensor): w [OC][C][R][R] ->
+// ws [OC][C*S*S][R'][R'], ws[oc][(c*S + dy)*S + dx][ky'][kx'] = w[oc][c][S*ky' + dy][S*kx' + dx] (0 past R).
+__global__ void __launch_bounds__(256) k_s2d_filters(const float* __restrict__ w, float* __restrict__ w2, int OC, int C,
+                                                     int R, int S, int R2) {
+    const int C2 = C * S * S;
+    const long long total = (long long)OC * C2 * R2 * R2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int kx2 = (int)(i % R2);
+        long long t = i / R2;
+        const int ky2 = (int)(t % R2);
+        t /= R2;
+        const int c2 = (int)(t % C2);
+        const int oc = (int)(t / C2);
+        const int dx = c2 % S, u = c2 / S, dy = u % S, c = u / S;
+        const int ky = S * ky2 + dy, kx = S * kx2 + dx;
+        w2[i] = (ky < R && kx < R) ? w[(((long long)oc * C + c) * R + ky) * R + kx] : 0.0f;
+    }
+}
+
 // x [N][C][H][W] (C <= 4) -> xp [N][Hp][Wp][4], image at (pad, pad), zeros
 // elsewhere: one thread per padded pixel, coalesced plane reads, float4 writes.
 __global__ void __launch_bounds__(256) k_to_nhwc4_pad(const float* __restrict__ x, float4* __restrict__ xp, int C,

@@ -282,13 +282,13 @@ class _UmmaFamily(Variant):
                 for split in (1, 2, 4, 8, 16, 32, 0):  # 0 = stream-K (TMA kernel)
                     if split > 1 and kblocks // split < 2:
                         continue
-                    for tma in ((1, 2, 3, 4, 5) if split == 0 else (1, 2, 3, 4, 5, 0)):  # 5: bf16 mode only
+                    for tma in ((1, 2, 3, 4, 5, 6) if split == 0 else (1, 2, 3, 4, 5, 6, 0)):  # 5: bf16 mode only; 6: first layers
                         out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma))
                         if tma and split and bn <= 64:  # two CTAs per SM
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, occ=2))
                         if tma in (1, 2) and split and bn >= 64 and not swap:  # CTA pairs multicasting filters
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=2))
-                        if (tma in (1, 3, 4) and bn in (64, 96, 128, 192) or tma == 5 and bn in (128, 192)) and not swap:  # 2-SM UMMA pairs (M = 256)
+                        if (tma in (1, 3, 4, 6) and bn in (64, 96, 128, 192) or tma == 5 and bn in (128, 192)) and not swap:  # 2-SM UMMA pairs (M = 256)
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=3))
                         if 2 <= split <= 8 and tma in (1, 3, 4) and (bn in (32, 64) and not swap or bn == 32 and swap):
                             out.append(TuneParams(bn=bn, split_k=split, swap_ab=swap, tma=tma, cl=4))  # split-K cluster

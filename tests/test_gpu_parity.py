@@ -69,7 +69,9 @@ def _variant_params(g):
                     TuneParams(bn=128, tma=3, cl=3), TuneParams(bn=128, split_k=0, tma=1, cl=3), TuneParams(bn=96, tma=1, cl=3),
                     TuneParams(bn=64, split_k=0, tma=4, cl=3), TuneParams(bn=32, split_k=2, tma=1, cl=4),
                     TuneParams(bn=64, split_k=4, tma=1, cl=4), TuneParams(bn=32, split_k=3, tma=3, cl=4),
-                    TuneParams(bn=64, split_k=2, tma=4, cl=4), TuneParams(bn=32, swap_ab=True, split_k=4, tma=1, cl=4)):
+                    TuneParams(bn=64, split_k=2, tma=4, cl=4), TuneParams(bn=32, swap_ab=True, split_k=4, tma=1, cl=4),
+                    TuneParams(bn=96, tma=6), TuneParams(bn=64, split_k=2, tma=6), TuneParams(bn=96, tma=6, cl=3),
+                    TuneParams(bn=128, split_k=0, tma=6)):
             out.append((v, prm))
     out += [("conv_wino", p) for p in (TuneParams(bn=64, tma=1), TuneParams(bn=128, split_k=2, tma=1),
                                        TuneParams(bn=192, split_k=0, tma=1), TuneParams(bn=64, swap_ab=True, tma=1),
@@ -340,3 +342,40 @@ def test_batch_slabs_concatenate_bit_identical(cuda, row, params):
         parts.append(o.y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, 0), whole.y)
+
+
+@pytest.mark.parametrize("row,batch,params", [(34, 20, "BN=96,sk=1,sw=0,dr=0,tm=6"), (33, 5, "BN=96,sk=1,sw=0,dr=0,tm=6,cl=3"),
+                                              (35, 20, "BN=64,sk=1,sw=0,dr=0,tm=6"), (34, 1, "BN=32,sk=4,sw=0,dr=0,tm=6"),
+                                              (35, 5, "BN=64,sk=0,sw=0,dr=0,tm=6")])
+def test_first_layer_space_to_depth_full_size(cuda, row, batch, params):
+    """tma=6: AlexNet / NiN / GoogLeNet conv1 as R'xR' stride-1 convs over a space-to-depth copy of x
+    (C*S*S channels, re-arranged filters): same fp32-exact products, so the reference tolerance holds;
+    also on signed data with exact ReLU clipping."""
+    import torch
+
+    from paper_1611_06945_b200 import corpus, runner
+    from paper_1611_06945_b200.frontend import with_fused
+    from paper_1611_06945_b200.variants import VARIANTS, TuneParams
+
+    op = corpus.corpus(batch)[row]
+    g = with_fused(op.graph(), "conv", "relu")
+    node = g.node("conv")
+    p = TuneParams.from_string("MNt=4:4,MNb=16:16,Kb=4,vw=4,lf=1,li=1," + params)
+    plan = VARIANTS["conv_umma"].generate(node, g.edges, p)
+    for low, high in ((0.1, 1.0), (-1.0, 1.0)):
+        x, f, b = conv_ref.conv_inputs(op.batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz,
+                                       f"s2d:{row}:{batch}:{low}", low=low, high=high)
+        cop = runner.ConvOp(plan, *(torch.from_numpy(a).cuda() for a in (x, f, b)))
+        cop.y.fill_(float("nan"))
+        cop.launch()
+        torch.cuda.synchronize()
+        got = cop.y.cpu().numpy()
+        if low > 0:
+            want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
+            res = conv_ref.compare(got, want, conv_ref.tolerance_for(op.in_chans * op.ksz * op.ksz))
+            assert res.ok, res
+        else:
+            pre = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=False).astype(np.float64)
+            bound = 1e-5 * conv_ref.signed_bound(x, f, op.stride, op.pad) + 1e-6
+            assert (np.abs(got.astype(np.float64) - np.maximum(pre, 0.0)) <= bound).all()
+            assert (got[pre < -bound] == 0.0).all()
