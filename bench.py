@@ -233,6 +233,42 @@ def measure_tf32_peak(dev, reps: int = 10) -> float:
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
+def measure_pcie(dev, nbytes: int = 1 << 28, reps: int = 3) -> dict:
+    """Pinned-host copy bandwidth (GB/s): H2D alone, D2H alone, and each direction
+    while both run at once -- the denominator of the e2e copy bound."""
+    import torch
+
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    cur = torch.cuda.current_stream(dev)
+    out = {}
+    for name in ("h2d", "d2h", "both"):
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(cur)
+            s_h2d.wait_event(e0)
+            s_d2h.wait_event(e0)
+            if name != "d2h":
+                with torch.cuda.stream(s_h2d):
+                    d_in.copy_(h_in, non_blocking=True)
+            if name != "h2d":
+                with torch.cuda.stream(s_d2h):
+                    h_out.copy_(d_out, non_blocking=True)
+            cur.wait_stream(s_h2d)
+            cur.wait_stream(s_d2h)
+            e1.record(cur)
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e1))
+        out[name + "_gbs"] = round(nbytes / (best * 1e-3) / 1e9, 2)
+    del h_in, h_out, d_in, d_out
+    return out
+
+
 def build_sweep(batches, db, heuristic, prec=0):
     """(row, BenchOp, node, edges, variant, params) for every unit of the sweep."""
     from paper_1611_06945_b200 import corpus
@@ -663,9 +699,14 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
             tt = tt.cpu() if one_gpu_test else tt
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())
+        h2d_b, d2h_b = sum(h.h2d_bytes for h in hosts), sum(h.d2h_bytes for h in hosts)
+        pcie = measure_pcie(dev)
+        # copy bound: both directions stream concurrently at the measured duplex rate
+        copy_ms = max(h2d_b / (pcie["both_gbs"] * 1e9), d2h_b / (pcie["both_gbs"] * 1e9)) * 1e3
         e2e = {"value": round(flops_all / (e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s", "ms_per_step": round(e_ms, 3),
-               "h2d_bytes_per_step": sum(h.h2d_bytes for h in hosts),
-               "d2h_bytes_per_step": sum(h.d2h_bytes for h in hosts), "steps": ksteps,
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": ksteps,
+               "pcie_measured": pcie, "copy_bound_ms": round(copy_ms, 3),
+               "frac_of_copy_bound": round(copy_ms / e_ms, 4),
                "path": f"b2c_conv_fwd_host per op (pinned H2D x/w/bias + filter pack + kernel + D2H y), "
                        f"ops round-robin on {E2E_STREAMS} streams" + (" (bytes: rank 0's share)" if world > 1 else "")}
 

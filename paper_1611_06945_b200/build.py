@@ -25,10 +25,16 @@ HEADER = os.path.join(INCLUDE, "b2conv.h")
 def units() -> dict:
     """object name -> (main .cu, every source it depends on)."""
     cuh = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cuh")]
-    return {
+    out = {
         "b2conv.o": (os.path.join(CSRC, "b2conv.cu"), [os.path.join(CSRC, "b2conv.cu"), HEADER, *cuh]),
         "b2net.o": (os.path.join(CSRC, "b2net.cu"), [os.path.join(CSRC, "b2net.cu"), HEADER]),
     }
+    # k_tconv instances, one translation unit per MODE (tconv_inst.cuh)
+    for f in sorted(os.listdir(CSRC)):
+        if f.startswith("inst_m") and f.endswith(".cu"):
+            src = os.path.join(CSRC, f)
+            out[f[:-3] + ".o"] = (src, [src, HEADER, *cuh])
+    return out
 
 
 def sources() -> list:
@@ -86,15 +92,25 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     os.makedirs(OBJDIR, exist_ok=True)
-    objs = []
+    objs, todo = [], []
     for name, (main, deps) in units().items():
         obj = os.path.join(OBJDIR, name)
         if force or not _newer(obj, deps):
-            digest = _digest(deps)  # of the sources as compiled (taken before nvcc reads them)
-            _run([nvcc, *NVCC_FLAGS, "-c", "-o", obj + ".tmp", main], verbose)
-            os.replace(obj + ".tmp", obj)
-            _write_stamp(obj, digest)
+            todo.append((obj, main, _digest(deps)))  # digest of the sources as compiled (before nvcc reads them)
         objs.append(obj)
+
+    def compile_one(job):
+        obj, main, digest = job
+        _run([nvcc, *NVCC_FLAGS, "-c", "-o", obj + ".tmp", main], verbose)
+        os.replace(obj + ".tmp", obj)
+        _write_stamp(obj, digest)
+
+    # the translation units are independent: compile them in parallel (nvcc is single-threaded)
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        for _ in ex.map(compile_one, todo):
+            pass
     digest = _digest(sources())
     if any(not _newer(o, d) for o, (_, d) in zip(objs, units().values())):
         raise RuntimeError("sources changed during the build; run it again")

@@ -21,6 +21,11 @@
 #include "k_tma.cuh"
 #include "k_fcs.cuh"
 #include "k_wino.cuh"
+#include "tconv_inst.cuh"
+
+namespace b2c {
+__device__ long long g_b2c_trace[256];  // phase trace of k_tconv CTA 0 (debug; TArgs.trace_buf points here)
+}  // namespace b2c
 
 using namespace b2c;
 
@@ -140,7 +145,7 @@ bool s2d_of(const b2c_conv_desc* d, const b2c_tune* t, S2d& o) {
 int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why);
 
 int applies_s2d(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
-    if (t->variant != B2C_VAR_UMMA || d->prec != B2C_PREC_FP32) { why = "tma=6 (first-layer space-to-depth): conv_umma, fp32-exact"; return B2C_INAPPLICABLE; }
+    if (t->variant != B2C_VAR_UMMA) { why = "tma=6 (first-layer space-to-depth): conv_umma"; return B2C_INAPPLICABLE; }
     if (d->c > 4 || (d->stride != 2 && d->stride != 4) || d->r <= d->stride || (d->c * d->stride * d->stride) % 4 ||
         d->c * d->stride * d->stride <= 4) {
         why = "tma=6: first layers (C <= 4) with stride 2 or 4 < ksz and C*stride^2 a multiple of 4 above 4"; return B2C_INAPPLICABLE;
@@ -555,6 +560,11 @@ using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 int g_trace_on = 0;
+long long* trace_buf() {  // device address of g_b2c_trace (looked up when tracing is on)
+    long long* p = nullptr;
+    if (g_trace_on & 15) cudaGetSymbolAddress(reinterpret_cast<void**>(&p), b2c::g_b2c_trace);
+    return p;
+}
 std::once_flag g_drv_once;
 EncodeTiledFn g_enc_tiled = nullptr;
 EncodeIm2colFn g_enc_im2col = nullptr;
@@ -673,111 +683,6 @@ void set_unit_divs(TArgs& a) {
     a.fTilesX = FastDiv((uint32_t)std::max(1, a.tiles_x));
 }
 
-using TconvKernel = void (*)(const CUtensorMap, const CUtensorMap, TArgs);
-
-struct TconvEntry {
-    TconvKernel fn;
-    int smem;
-    int threads;
-};
-
-template <int BN, bool SWAP, int MODE, int OCC, int CL, int PREC = 0>
-TconvEntry tconv_entry() {
-    using C = TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>;
-    return TconvEntry{&k_tconv<BN, SWAP, MODE, OCC, CL, PREC>, C::SMEM, C::THREADS};
-}
-
-template <int MODE>
-TconvEntry tconv_pick_bf16(int bn) {
-    switch (bn) {
-        case 32: return tconv_entry<32, false, MODE, 1, 1, 1>();
-        case 64: return tconv_entry<64, false, MODE, 1, 1, 1>();
-        case 128: return tconv_entry<128, false, MODE, 1, 1, 1>();
-        case 192: return tconv_entry<192, false, MODE, 1, 1, 1>();
-    }
-    return TconvEntry{nullptr, 0, 0};
-}
-
-template <int MODE>
-TconvEntry tconv_pick_fp8(int bn) {
-    switch (bn) {
-        case 32: return tconv_entry<32, false, MODE, 1, 1, 2>();
-        case 64: return tconv_entry<64, false, MODE, 1, 1, 2>();
-        case 128: return tconv_entry<128, false, MODE, 1, 1, 2>();
-    }
-    return TconvEntry{nullptr, 0, 0};
-}
-
-template <bool SWAP, int MODE>
-TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
-    if (cl == 2) {
-        if constexpr (!SWAP && MODE != 1 && MODE != 5 && MODE != 6) {
-            switch (bn) {
-                case 64: return tconv_entry<64, false, MODE, 1, 2>();
-                case 96: return tconv_entry<96, false, MODE, 1, 2>();
-                case 128: return tconv_entry<128, false, MODE, 1, 2>();
-                case 192: return tconv_entry<192, false, MODE, 1, 2>();
-            }
-        }
-        return TconvEntry{nullptr, 0, 0};
-    }
-    if (cl == 4) {  // split-K clusters (DSMEM fixup)
-        if constexpr (!SWAP && (MODE == 0 || MODE == 5 || MODE == 6)) {
-            switch (bn) {
-                case 32: return tconv_entry<32, false, MODE, 1, 4>();
-                case 64: return tconv_entry<64, false, MODE, 1, 4>();
-            }
-        }
-        if constexpr (SWAP && MODE == 1) {
-            if (bn == 32) return tconv_entry<32, true, 1, 1, 4>();
-        }
-        return TconvEntry{nullptr, 0, 0};
-    }
-    if (cl == 3) {  // 2-SM UMMA pairs
-        if constexpr (!SWAP && MODE != 1 && MODE != 2 && MODE != 3) {
-            switch (bn) {
-                case 64: return tconv_entry<64, false, MODE, 1, 3>();
-                case 96: return tconv_entry<96, false, MODE, 1, 3>();
-                case 128: return tconv_entry<128, false, MODE, 1, 3>();
-                case 192: return tconv_entry<192, false, MODE, 1, 3>();
-            }
-        }
-        return TconvEntry{nullptr, 0, 0};
-    }
-    if (occ == 2) {
-        switch (bn) {
-            case 32: return tconv_entry<32, SWAP, MODE, 2, 1>();
-            case 64: return tconv_entry<64, SWAP, MODE, 2, 1>();
-        }
-        return TconvEntry{nullptr, 0, 0};
-    }
-    switch (bn) {
-        case 32: return tconv_entry<32, SWAP, MODE, 1, 1>();
-        case 64: return tconv_entry<64, SWAP, MODE, 1, 1>();
-        case 96: return tconv_entry<96, SWAP, MODE, 1, 1>();
-        case 128: return tconv_entry<128, SWAP, MODE, 1, 1>();
-        case 192: return tconv_entry<192, SWAP, MODE, 1, 1>();
-    }
-    return TconvEntry{nullptr, 0, 0};
-}
-
-template <int MODE>
-TconvEntry tconv_pick_sw(int bn, int swap, int occ, int cl) {
-    return swap ? tconv_pick_bn<true, MODE>(bn, occ, cl) : tconv_pick_bn<false, MODE>(bn, occ, cl);
-}
-
-TconvEntry tconv_pick(int bn, int swap, int mode, int occ, int cl) {
-    switch (mode) {
-        case 0: return tconv_pick_sw<0>(bn, swap, occ, cl);
-        case 1: return tconv_pick_sw<1>(bn, swap, occ, cl);
-        case 2: return tconv_pick_sw<2>(bn, swap, occ, cl);
-        case 3: return tconv_pick_sw<3>(bn, swap, occ, cl);
-        case 4: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 4>(bn, occ, cl);
-        case 5: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 5>(bn, occ, cl);
-        case 6: return swap ? TconvEntry{nullptr, 0, 0} : tconv_pick_bn<false, 6>(bn, occ, cl);
-    }
-    return TconvEntry{nullptr, 0, 0};
-}
 
 int num_sms() {
     static int n = 0;
@@ -799,22 +704,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     const int mode = t->tma == 5 ? 8 : t->tma == 4 ? 6 : t->tma == 3 ? 5 : p.kmode == 2 ? 1 : p.kmode == 5 ? 4 : p.kmode == 4 ? 3 : (plain_1x1 && t->tma == 2) ? 2 : 0;
     const int occ = t->stages == 2 ? 2 : 1;  // TMA kernel: b2c_tune.stages = CTAs per SM
     const int cl = (t->cluster >= 2 && t->cluster <= 4) ? t->cluster : 1;
-    TconvEntry e{nullptr, 0, 0};
-    if (d->prec == B2C_PREC_BF16)
-        e = mode == 0 ? tconv_pick_bf16<0>(t->tile_n) : mode == 2 ? tconv_pick_bf16<2>(t->tile_n)
-            : mode == 4 ? tconv_pick_bf16<4>(t->tile_n) : mode == 5 ? tconv_pick_bf16<5>(t->tile_n)
-            : mode == 6 ? tconv_pick_bf16<6>(t->tile_n)
-            : mode == 8 ? (cl == 3 ? (t->tile_n == 128 ? tconv_entry<128, false, 8, 1, 3, 1>()
-                                      : t->tile_n == 192 ? tconv_entry<192, false, 8, 1, 3, 1>()
-                                                         : TconvEntry{nullptr, 0, 0})
-                                   : tconv_pick_bf16<8>(t->tile_n))
-            : TconvEntry{nullptr, 0, 0};
-    else if (d->prec == B2C_PREC_FP8)
-        e = mode == 0 ? tconv_pick_fp8<0>(t->tile_n) : mode == 4 ? tconv_pick_fp8<4>(t->tile_n)
-            : mode == 5 ? tconv_pick_fp8<5>(t->tile_n) : mode == 6 ? tconv_pick_fp8<6>(t->tile_n)
-            : TconvEntry{nullptr, 0, 0};
-    else
-        e = tconv_pick(t->tile_n, t->swap_ab, mode, occ, cl);
+    const TconvEntry e = tconv_pick_mode(mode, d->prec, t->tile_n, t->swap_ab, occ, cl);
     if (!e.fn) return fail(B2C_INAPPLICABLE, "no TMA tcgen05 kernel for this tile");
     rc = ensure_smem_attr((const void*)e.fn, e.smem);
     if (rc) return rc;
@@ -921,6 +811,7 @@ int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const 
     a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
     a.ws = reinterpret_cast<float*>(wsb + p.part_off);
     a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
+    a.trace_buf = trace_buf();
     a.trace = g_trace_on & 15;  // bit0 trace, bit1 hi*hi only, bit2 no B split, bit3 no A->TMEM (experiments)
     a.relayout = (g_trace_on & 16) ? 0 : relayout;
     a.x = x;
@@ -1011,22 +902,6 @@ WinoPlan wino_plan(const b2c_conv_desc* d, const b2c_tune* t) {
     return p;
 }
 
-TconvEntry wino_pick(int bn, int swap) {
-    if (swap) {
-        switch (bn) {
-            case 64: return tconv_entry<64, true, 7, 1, 1>();
-            case 128: return tconv_entry<128, true, 7, 1, 1>();
-            case 192: return tconv_entry<192, true, 7, 1, 1>();
-        }
-    } else {
-        switch (bn) {
-            case 64: return tconv_entry<64, false, 7, 1, 1>();
-            case 128: return tconv_entry<128, false, 7, 1, 1>();
-            case 192: return tconv_entry<192, false, 7, 1, 1>();
-        }
-    }
-    return TconvEntry{nullptr, 0, 0};
-}
 
 int wino_filter_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* w, void* ws, size_t ws_bytes,
                      cudaStream_t st) {
@@ -1043,7 +918,7 @@ int wino_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
     if (!ws || ws_bytes < p.ws_bytes) return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
     int rc = load_tma_encoders();
     if (rc) return rc;
-    TconvEntry e = wino_pick(t->tile_n, t->swap_ab);
+    TconvEntry e = tconv_pick_mode(7, B2C_PREC_FP32, t->tile_n, t->swap_ab, 1, 1);
     if (!e.fn) return fail(B2C_INAPPLICABLE, "no Winograd GEMM kernel for this tile");
     rc = ensure_smem_attr((const void*)e.fn, e.smem);
     if (rc) return rc;
@@ -1099,6 +974,7 @@ int wino_fwd(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
         a.drain = t->drain > 0 ? std::max(2, t->drain) : 4;
         a.ws = reinterpret_cast<float*>(wsb + p.part_off);
         a.sems = reinterpret_cast<int*>(wsb + p.sems_off);
+        a.trace_buf = trace_buf();
         a.trace = g_trace_on & 15;
         a.kb_period = p.kblocks;
         a.ksteps_last = std::min(TM_BK / 8, std::max(1, (d->c - TM_BK * (p.kblocks - 1) + 7) / 8));

@@ -489,10 +489,10 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 // device array read back by b2c_debug_trace_read(); off unless TArgs.trace != 0.
 // Slots: 0-15 phases, 16+it split saw raw_full, 48+it split arrived, 80+it MMA
 // saw raw_full, 112+it MMA saw split_full, 144+it MMA committed, 176+it TMA issued (it < 32).
-__device__ long long g_b2c_trace[256];  // single translation unit (b2conv.cu)
+// (used inside k_tconv, whose TArgs `a` carries the buffer: g_b2c_trace of b2conv.cu)
 #define B2C_TRACE(on, slot)                                                           \
     do {                                                                              \
-        if ((on) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_b2c_trace[(slot)] = clock64(); \
+        if ((on) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) a.trace_buf[(slot)] = clock64(); \
     } while (0)
 
 // ----------------------------------------------------------------------------

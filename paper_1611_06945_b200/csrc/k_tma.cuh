@@ -178,6 +178,7 @@ struct TArgs {
     FastDiv fCB;        // MODE 0: channel blocks of 32 per filter tap
     int drain;
     int trace;          // debug: phase clocks of CTA 0 into g_b2c_trace
+    long long* trace_buf;  // debug: where (b2conv.cu's g_b2c_trace)
     // In-kernel re-layout of x (instead of a separate conversion launch):
     // 0 none (x already converted / fc), 1 NCHW -> NHWC (C channels),
     // 2 NCHW -> zero-padded NHWC4 [N][hp][wp][4] (first layers).
@@ -303,6 +304,7 @@ __device__ __forceinline__ bool next_unit(const TArgs& a, UnitCursor& cur, int u
 }
 
 // ----------------------------------------------------------------------------- NCHW -> NHWC
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // x [N][C][HW] -> xh [N][HW][Cp] (Cp >= C, channels C..Cp-1 zero); 32x32 tiles
 // through shared memory so the read (along pixels) and the write (along
@@ -329,6 +331,8 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
         if (p < HW && c < Cp) dst[(size_t)p * Cp + c] = tile[tx][j];
     }
 }
+#endif
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // bf16 mode, MODE 8: x [N][C][HW] fp32 -> xh [N][HW][C] bf16 (round to nearest even, the
 // rounding the split pass of the TS path applies); same 32x32 smem tiles, 2-byte stores.
@@ -354,6 +358,7 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc_bf16(const float* __restri
         if (p < HW && c < C) dst[(size_t)p * C + c] = (uint16_t)(pack_bf16x2(tile[tx][j], 0.0f) & 0xFFFFu);
     }
 }
+#endif
 
 // First layers, space-to-depth (tm=6): x [N][C][H][W] -> xs [N][H'][W'][C*S*S] with
 // xs[n][Y][X][(c*S + dy)*S + dx] = x[n][c][S*Y + dy - P][S*X + dx - P] (0 outside): an
@@ -386,6 +391,7 @@ __global__ void __launch_bounds__(256) k_s2d_nhwc(const float* __restrict__ x, f
         for (int q = 0; q < S * S / 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
 }
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // The matching filter transform (once per filter tensor): w [OC][C][R][R] ->
 // ws [OC][C*S*S][R'][R'], ws[oc][(c*S + dy)*S + dx][ky'][kx'] = w[oc][c][S*ky' + dy][S*kx' + dx] (0 past R).
@@ -405,6 +411,8 @@ __global__ void __launch_bounds__(256) k_s2d_filters(const float* __restrict__ w
         w2[i] = (ky < R && kx < R) ? w[(((long long)oc * C + c) * R + ky) * R + kx] : 0.0f;
     }
 }
+#endif
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // x [N][C][H][W] (C <= 4) -> xp [N][Hp][Wp][4], image at (pad, pad), zeros
 // elsewhere: one thread per padded pixel, coalesced plane reads, float4 writes.
@@ -433,6 +441,7 @@ __global__ void __launch_bounds__(256) k_to_nhwc4_pad(const float* __restrict__ 
         dst[xq] = v;
     }
 }
+#endif
 
 // ----------------------------------------------------------------------------- fused re-layout
 
@@ -446,7 +455,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // then all CTAs meet at a grid barrier (grid <= #SMs with one CTA per SM, so
 // all CTAs are co-resident).  Saves a kernel boundary per op.  `scratch` is
 // the (still unused) pipeline smem: a 32 x 33 transpose tile per warp.
-__device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
+static __device__ void fused_relayout(const TArgs& a, uint8_t* scratch) {
     const Geom& g = a.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     if (a.relayout == 1) {

@@ -261,6 +261,7 @@ __device__ __forceinline__ float packed_k_value(const Geom& g, const float* __re
     const int k = kb * UMMA_BK + kk;
     return k < g.K ? w[(long long)oc * g.K + k] : 0.0f;
 }
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // bf16 pack for the TMA kernel's bf16 mode: [filter tile][K block][8-element chunk 0..3][rows][8 x bf16]
 // (UMMA no-swizzle K-major core matrices: 8 rows x 16 B contiguous), round to nearest even.
@@ -281,6 +282,8 @@ __global__ void __launch_bounds__(256) k_pack_filters_bf16(Geom g, const float* 
         out[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
     }
 }
+#endif
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // bf16 pack for MODE 8 (tm=5): per (filter tile, K block of 64 channels of one tap) the
 // SWIZZLE_128B K-major image the SS MMAs read: rows of 128 B (64 bf16), 16-byte chunk c
@@ -307,6 +310,8 @@ __global__ void __launch_bounds__(256) k_pack_filters_bf16_sw128(Geom g, const f
         out[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
     }
 }
+#endif
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 // e4m3 pack for the TMA kernel's fp8 mode: [filter tile][K block][16-element chunk 0..1][rows][16 x e4m3]
 // (UMMA no-swizzle K-major core matrices: 8 rows x 16 B contiguous), round to nearest even, saturating.
@@ -329,6 +334,8 @@ __global__ void __launch_bounds__(256) k_pack_filters_e4m3(Geom g, const float* 
         out[i] = (uint8_t)(two & 0xFF);
     }
 }
+#endif
+#ifndef B2C_INST_TU  // (non-template kernel: defined in b2conv.cu's translation unit only)
 
 __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __restrict__ w, float* __restrict__ out,
                                                       int rows, int kblocks, FastDiv fCB, int kmode,
@@ -382,6 +389,7 @@ __global__ void __launch_bounds__(256) k_pack_filters(Geom g, const float* __res
         }
     }
 }
+#endif
 
 // --------------------------------------------------------------------------- main kernel
 

@@ -42,7 +42,7 @@ def _params():
             TuneParams(bn=128, split_k=2, tma=3, prec=1), TuneParams(bn=64, tma=5, prec=1),
             TuneParams(bn=128, split_k=2, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, prec=1),
             TuneParams(bn=128, tma=5, cl=3, prec=1), TuneParams(bn=192, split_k=2, tma=5, cl=3, prec=1),
-            TuneParams(bn=128, split_k=0, tma=5, cl=3, prec=1)]
+            TuneParams(bn=128, split_k=0, tma=5, cl=3, prec=1), TuneParams(bn=64, split_k=1, tma=6, prec=1)]
 
 
 def _graph(c, relu):
@@ -70,7 +70,7 @@ def test_bf16_golden_cases(cuda, case):
         assert ran > 0
 
 
-@pytest.mark.parametrize("row,batch", [(42, 20), (34, 5), (2, 20), (40, 5), (35, 1), (20, 5)])
+@pytest.mark.parametrize("row,batch", [(42, 20), (34, 5), (2, 20), (40, 5), (35, 1), (20, 5), (33, 20), (35, 20)])
 def test_bf16_full_size_signed(cuda, row, batch):
     from paper_1611_06945_b200 import corpus
     from paper_1611_06945_b200.variants import TuneParams
@@ -83,10 +83,14 @@ def test_bf16_full_size_signed(cuda, row, batch):
     want = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True)
     bound = conv_ref.signed_bound(x, f, op.stride, op.pad)
     for p in (TuneParams(bn=64, tma=1, prec=1), TuneParams(bn=128, split_k=0, tma=1, prec=1),
-              TuneParams(bn=128, split_k=0, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, cl=3, prec=1)):
+              TuneParams(bn=128, split_k=0, tma=5, prec=1), TuneParams(bn=192, split_k=0, tma=5, cl=3, prec=1),
+              TuneParams(bn=64, split_k=1, tma=6, prec=1), TuneParams(bn=128, split_k=0, tma=6, prec=1)):
         got = _run(g, x, f, b, p)
         if got is None and p.tma == 5:  # the bf16-NHWC SS path needs in_chans % 8 == 0 (not first layers)
             assert op.in_chans % 8 or op.in_chans <= 4
+            continue
+        if got is None and p.tma == 6:  # space-to-depth: strided first layers only
+            assert op.in_chans > 4 or op.stride == 1
             continue
         assert got is not None
         err = np.abs(got.astype(np.float64) - want.astype(np.float64))

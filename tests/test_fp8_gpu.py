@@ -85,7 +85,9 @@ def _abs_sum_bound(x, f, stride, pad):
 
 @pytest.mark.parametrize("row,batch,ptxt", [(34, 1, "BN=64,sk=1,tm=1"), (42, 5, "BN=128,sk=0,tm=1"),
                                             (38, 20, "BN=64,sk=2,tm=1"), (9, 20, "BN=64,sk=1,tm=3"),
-                                            (41, 5, "BN=128,sk=1,tm=4"), (2, 1, "BN=32,sk=4,tm=1")])
+                                            (41, 5, "BN=128,sk=1,tm=4"), (2, 1, "BN=32,sk=4,tm=1"),
+                                            (34, 20, "BN=64,sk=1,tm=6"), (35, 5, "BN=128,sk=0,tm=6"),
+                                            (33, 1, "BN=32,sk=2,tm=6")])
 def test_fp8_signed_full_size(cuda, row, batch, ptxt):
     from paper_1611_06945_b200 import corpus
     from paper_1611_06945_b200.frontend import with_fused
