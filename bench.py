@@ -600,6 +600,31 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
                 for i in range(n):
                     per_op[i] += evs[i].elapsed_time(evs[i + 1]) / args.steps
 
+    # ---- per-op back-to-back: each op launched R times in one CUDA graph (what a launch costs
+    # when the next one queues behind it: no event nodes between launches, ~4 us each; the
+    # inputs stay L2-resident between launches except fc6's 151 MB of weights)
+    R_B2B = 8
+    per_op_b2b = [0.0] * n
+    for i, o in enumerate(ops):
+        gb2b = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(main):
+            with torch.cuda.graph(gb2b, stream=main):
+                for _ in range(R_B2B):
+                    o.launch(main.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gb2b.replay()
+        best = float("inf")
+        for _ in range(3):
+            with torch.cuda.stream(main):
+                e0.record(main)
+                gb2b.replay()
+                e1.record(main)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / R_B2B)
+        per_op_b2b[i] = best
+        del gb2b
+    torch.cuda.synchronize()
+
     # ---- the timed step: one group per batch size (the same groups on every rank), each one
     # CUDA graph over concurrent branches; shard mode: after a group, its slabs go to rank 0
     # (NCCL p2p on NCCL's stream, overlapping the next group's compute)
@@ -759,7 +784,7 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     for i, (row, op, vname, params, sig, it) in enumerate(r[:6] for r in rows):
         fl_i, by_i = conv_flops(ops[i].plan.desc), conv_bytes(ops[i].plan.desc)
         per_rows.append([row, op.batch, round(per_op[i] * 1e3, 2), round(fl_i / per_op[i] / 1e9, 2),
-                         round(frac_of_roof(fl_i, by_i, per_op[i]), 4)])
+                         round(frac_of_roof(fl_i, by_i, per_op[i]), 4), round(per_op_b2b[i] * 1e3, 2)])
     if args.per_op_out:
         with open(args.per_op_out, "w") as fh:
             fh.write("row,batch,signature,variant,params,ms,tflops,gbs,flops,bytes,frac_roofline,sweep_variant,sweep_params\n")
@@ -791,9 +816,10 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
         cpu = cpu_baseline(batches, args.cpu_seconds)
     by_batch = {}
     for i, (row, op, vname, params, sig, it) in enumerate(r[:6] for r in rows):
-        e = by_batch.setdefault(sweep[it.unit][1].batch, [0.0, 0])
+        e = by_batch.setdefault(sweep[it.unit][1].batch, [0.0, 0, 0.0])
         e[0] += per_op[i]
         e[1] += conv_flops(ops[i].plan.desc)
+        e[2] += per_op_b2b[i]
     roof_ms_mine = sum(frac_of_roof(conv_flops(o.plan.desc), conv_bytes(o.plan.desc), per_op[i]) * per_op[i]
                        for i, o in enumerate(ops))
     line = {
@@ -821,12 +847,16 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
                    "group_ms": {("batch " + str(g[0]) if per_batch else "all"): round(ms, 4) for g, ms in zip(groups, group_ms)},
                    "per_batch_ms_isolated": {str(k): round(v[0], 4) for k, v in sorted(by_batch.items())},
                    "per_batch_tflops_isolated": {str(k): round(v[1] / v[0] / 1e9, 2) for k, v in sorted(by_batch.items())},
+                   "per_batch_ms_back_to_back": {str(k): round(v[2], 4) for k, v in sorted(by_batch.items())},
+                   "per_op_timing": ("us: isolated (serial graph, an event node after every op: ~4 us of event "
+                                     "overhead included); us_b2b: the op launched 8x back to back in one graph "
+                                     "(launch gaps included, inputs L2-warm except fc6)"),
                    "serial_ms_per_step_rank0": round(sum(per_op), 4),
                    "roofline_ms_rank0": round(roof_ms_mine, 4),
                    "frac_roofline_step": round(roof_ms_mine / ms_step, 4) if world == 1 else None,
                    **configs},
         "roofline": roof,
-        "per_op": {"cols": ["row", "n", "us", "tflops", "frac_roofline"], "rows": per_rows},
+        "per_op": {"cols": ["row", "n", "us", "tflops", "frac_roofline", "us_b2b"], "rows": per_rows},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_mine * args.steps,

@@ -233,9 +233,10 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             if (!(d->r == d->h && d->r == d->w && d->pad == 0 && d->oh == 1 && d->ow == 1)) {
                 why = "filters must cover the whole input with 1x1 output"; return B2C_INAPPLICABLE;
             }
-            if (t->kb != 1 && t->kb != 2) { why = "Kb must be 1 (x from L1/L2) or 2 (x staged in smem)"; return B2C_INAPPLICABLE; }
-            if (d->n > (t->kb == 2 ? 32 : 8)) { why = "weight streaming is for batch <= 8 (Kb=1) / <= 32 (Kb=2)"; return B2C_INAPPLICABLE; }
+            if (t->kb < 1 || t->kb > 3) { why = "Kb must be 1 (x from L1/L2), 2 (x staged in smem) or 3 (TMA bulk ring)"; return B2C_INAPPLICABLE; }
+            if (d->n > (t->kb == 2 ? 32 : 8)) { why = "weight streaming is for batch <= 8 (Kb=1|3) / <= 32 (Kb=2)"; return B2C_INAPPLICABLE; }
             if ((d->c * d->r * d->r) % 4) { why = "ic*h*w % 4 != 0 (16-byte rows)"; return B2C_INAPPLICABLE; }
+            if (t->kb == 3) return B2C_OK;  // fixed shape: 8 compute warps, rows per CTA from OC / SMs
             if (t->mnb0 != 2 && t->mnb0 != 4 && t->mnb0 != 8) { why = "warps per block (MNb0) must be 2, 4 or 8"; return B2C_INAPPLICABLE; }
             if (t->kb == 1 && t->mnt1 != 2 && t->mnt1 != 4 && t->mnt1 != 8) { why = "rows per block (MNt1) must be 2, 4 or 8"; return B2C_INAPPLICABLE; }
             if (t->kb == 2 && t->mnt1 != 1 && t->mnt1 != 2 && t->mnt1 != 4) { why = "rows per warp (MNt1) must be 1, 2 or 4"; return B2C_INAPPLICABLE; }
@@ -695,6 +696,12 @@ int num_sms() {
     return n;
 }
 
+// k_fc_bulk: out_chan rows per CTA (one CTA per SM, <= 32 rows: 4 per compute warp)
+int fcb_rows_per_cta(int oc) {
+    const int sms = num_sms();
+    return std::min(FCB_WARPS * FCB_MAX_RPW, std::max(1, (oc + sms - 1) / sms));
+}
+
 int tma_fwd(const b2c_conv_desc* d, const b2c_tune* t, const UmmaPlan& p, const Geom& g, const float* x,
             const float* w, const float* bias, float* y, void* ws, cudaStream_t st,
             const b2c_conv_desc* s2d_src = nullptr) {  // s2d_src: the original first-layer conv (tma = 6)
@@ -1042,6 +1049,21 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
             break;
         case B2C_VAR_FC_STREAM: {
             using FcsKernel = void (*)(const float*, const float*, const float*, float*, int, int, int, int);
+            if (t->kb == 3) {  // TMA bulk ring (k_fc_bulk)
+                using FcbKernel = void (*)(const float*, const float*, const float*, float*, int, int, int, int, int, int);
+                const int nb = d->n <= 1 ? 1 : d->n <= 2 ? 2 : d->n <= 4 ? 4 : 8;
+                FcbKernel fn = nb == 1 ? k_fc_bulk<1> : nb == 2 ? k_fc_bulk<2> : nb == 4 ? k_fc_bulk<4> : k_fc_bulk<8>;
+                const int rpc = fcb_rows_per_cta(g.OC);
+                const int stage_bytes = (rpc + g.N) * FCB_KC * (int)sizeof(float);
+                const int nst = std::min(8, (TM_MAX_SMEM - FCB_HDR) / stage_bytes);
+                if (nst < 2) return fail(B2C_INAPPLICABLE, "k_fc_bulk: fewer than two stages fit");
+                const int sm = FCB_HDR + nst * stage_bytes;
+                rc = ensure_smem_attr((const void*)fn, sm);
+                if (rc) return rc;
+                const int nblocks = (g.OC + rpc - 1) / rpc;
+                fn<<<std::min(nblocks, num_sms()), 32 * (FCB_WARPS + 1), sm, st>>>(x, w, bias, y, g.N, g.OC, g.K, g.act, rpc, nst);
+                break;
+            }
             if (t->kb == 2) {
                 const int nb = d->n <= 1 ? 1 : d->n <= 2 ? 2 : d->n <= 4 ? 4 : d->n <= 8 ? 8 : d->n <= 16 ? 16 : d->n <= 20 ? 20 : 32;
                 const int R = t->mnt1;
@@ -1346,6 +1368,10 @@ int b2c_conv_grid(const b2c_conv_desc* d, const b2c_tune* t) {
             return p.streamk ? p.sk_grid : (int)std::min<long long>(p.units, num_sms());
         }
         case B2C_VAR_FC_STREAM:
+            if (t->kb == 3) {
+                const int rpc = fcb_rows_per_cta(g.OC);
+                return std::min((g.OC + rpc - 1) / rpc, num_sms());
+            }
             return t->kb == 2 ? (g.OC + t->mnb0 * t->mnt1 - 1) / (t->mnb0 * t->mnt1) : (g.OC + t->mnt1 - 1) / t->mnt1;
         default: {
             S2d o;

@@ -175,4 +175,127 @@ __global__ void __launch_bounds__(256) k_fc_smem(const float* __restrict__ x, co
     }
 }
 
+// Kb = 3 form (batch <= 8): the weight rows are streamed by the TMA engine
+// (cp.async.bulk, one 2 KB copy per row per K chunk) into a deep shared-memory
+// ring, so each SM keeps ~150 KB of weights in flight -- the op is bound by HBM
+// latency x bytes in flight, which the register-staged loads of Kb = 1 / 2
+// cannot reach.  One CTA per SM owns a block of rpc <= 32 consecutive out_chan
+// rows (rows warp, warp + 8, ...: at most 4 per compute warp); a stage is the
+// block's rows and the N image rows over one 512-float K chunk, both read from
+// shared memory by the 8 compute warps (lane = float4 column, conflict-free).
+// A producer warp issues the copies; per-stage full / empty mbarriers.  Every
+// lane accumulates its rows x N sums over its K columns; a fixed shuffle tree
+// finishes each (deterministic).
+constexpr int FCB_KC = 512;     // floats of K per stage
+constexpr int FCB_WARPS = 8;    // compute warps (+1 producer warp)
+constexpr int FCB_MAX_RPW = 4;  // rows per compute warp: rpc <= 32
+constexpr int FCB_HDR = 128;    // barriers
+
+template <int NB>
+__global__ void __launch_bounds__(32 * (FCB_WARPS + 1), 1)
+    k_fc_bulk(const float* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
+              float* __restrict__ y, int N, int OC, int K, int act, int rpc, int nst) {
+    extern __shared__ __align__(128) uint8_t fsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(fsm);
+    uint64_t* empty = full + nst;
+    float* stg = reinterpret_cast<float*>(fsm + FCB_HDR);
+    const int stage_floats = (rpc + N) * FCB_KC;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nchunks = (K + FCB_KC - 1) / FCB_KC;
+    const int nblocks = (OC + rpc - 1) / rpc;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), FCB_WARPS);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == FCB_WARPS) {  // producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+                const int r0 = rb * rpc, nr = min(rpc, OC - r0);
+                for (int c = 0; c < nchunks; ++c) {
+                    mbar_wait(smem_u32(&empty[s]), ph ^ 1u);
+                    const int k0 = c * FCB_KC;
+                    const uint32_t bytes = (uint32_t)min(FCB_KC, K - k0) * 4u;
+                    const uint32_t bar = smem_u32(&full[s]);
+                    mbar_arrive_expect_tx(bar, bytes * (uint32_t)(nr + N));
+                    float* base = stg + (size_t)s * stage_floats;
+                    for (int r = 0; r < nr; ++r)
+                        bulk_g2s(smem_u32(base + r * FCB_KC), w + (size_t)(r0 + r) * K + k0, bytes, bar);
+                    for (int n = 0; n < N; ++n)
+                        bulk_g2s(smem_u32(base + (rpc + n) * FCB_KC), x + (size_t)n * K + k0, bytes, bar);
+                    if (++s == nst) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+        const int r0 = rb * rpc, nr = min(rpc, OC - r0);
+        float acc[FCB_MAX_RPW][NB];
+#pragma unroll
+        for (int j = 0; j < FCB_MAX_RPW; ++j)
+#pragma unroll
+            for (int n = 0; n < NB; ++n) acc[j][n] = 0.0f;
+        for (int c = 0; c < nchunks; ++c) {
+            mbar_wait(smem_u32(&full[s]), ph);
+            const float4* base = reinterpret_cast<const float4*>(stg + (size_t)s * stage_floats);
+            const int kl4 = min(FCB_KC, K - c * FCB_KC) >> 2;
+#pragma unroll
+            for (int i = 0; i < FCB_KC / 128; ++i) {
+                const int q = lane + 32 * i;
+                if (q >= kl4) break;
+                float4 xv[NB];
+#pragma unroll
+                for (int n = 0; n < NB; ++n)
+                    if (n < N) xv[n] = base[(rpc + n) * (FCB_KC / 4) + q];
+#pragma unroll
+                for (int j = 0; j < FCB_MAX_RPW; ++j) {
+                    const int r = warp + FCB_WARPS * j;
+                    if (r < nr) {
+                        const float4 wv = base[r * (FCB_KC / 4) + q];
+#pragma unroll
+                        for (int n = 0; n < NB; ++n) {
+                            if (n < N) {
+                                float a = acc[j][n];
+                                a = fmaf(wv.x, xv[n].x, a);
+                                a = fmaf(wv.y, xv[n].y, a);
+                                a = fmaf(wv.z, xv[n].z, a);
+                                a = fmaf(wv.w, xv[n].w, a);
+                                acc[j][n] = a;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+            if (++s == nst) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < FCB_MAX_RPW; ++j) {
+            const int r = warp + FCB_WARPS * j;
+#pragma unroll
+            for (int n = 0; n < NB; ++n) {
+                float v = acc[j][n];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0 && r < nr && n < N) y[(size_t)n * OC + r0 + r] = apply_act(v + __ldg(bias + r0 + r), act);
+            }
+        }
+    }
+}
+
 }  // namespace b2c

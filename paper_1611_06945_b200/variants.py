@@ -344,7 +344,9 @@ class ConvFCStream(Variant):
     small batch, where the op is HBM-bound.  Kb=1 (batch <= 8): warps split K,
     x read through L1/L2, MNb0 = warps per block (2|4|8), MNt1 = rows per block
     (2|4|8).  Kb=2 (batch <= 32): x staged in shared memory per block, MNb0 =
-    warps (4|8), MNt1 = rows per warp (1|2|4)."""
+    warps (4|8), MNt1 = rows per warp (1|2|4).  Kb=3 (batch <= 8): weights and
+    x streamed by TMA bulk copies into a deep shared-memory ring (k_fc_bulk, one
+    CTA per SM; MNb / MNt unused)."""
 
     name, rank, vid = "conv_fc_stream", 5, backend.VAR_FC_STREAM
 
@@ -356,6 +358,7 @@ class ConvFCStream(Variant):
             return []  # fp32-exact only
         out = [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=1, vw=1) for wp in (2, 4, 8) for r in (2, 4, 8)]
         out += [TuneParams(mnt=(1, r), mnb=(wp, 1), kb=2, vw=1) for wp in (4, 8) for r in (1, 2, 4)]
+        out.append(TuneParams(mnt=(1, 1), mnb=(8, 1), kb=3, vw=1))
         return [p for p in out if self.applies(node, edges, p) is None]
 
 

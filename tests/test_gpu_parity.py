@@ -250,6 +250,36 @@ def test_fc_stream_staged_full_size(cuda, row, batch):
         assert r.ok, (p.to_string(), r)
 
 
+@pytest.mark.parametrize("row,batch", [(25, 1), (25, 5), (13, 5), (13, 8), (25, 3), (13, 7)])
+def test_fc_bulk_full_size(cuda, row, batch):
+    """conv_fc_stream Kb=3 (k_fc_bulk: weights + x streamed by TMA bulk copies through a
+    shared-memory ring) on AlexNet fc6 / fc7: reference data at the fp32 tolerance, signed
+    data with exact ReLU clipping, and bit-identical reruns (fixed reduction order)."""
+    from paper_1611_06945_b200 import corpus
+    from paper_1611_06945_b200.variants import TuneParams
+
+    op = corpus.corpus(batch)[row]
+    c = {"ksz": op.ksz, "stride": op.stride, "pad": op.pad, "out_chans": op.out_chans,
+         "in": (batch, op.in_chans, op.in_y, op.in_x)}
+    g = _graph(c, True)
+    p = TuneParams(mnt=(1, 1), mnb=(8, 1), kb=3, vw=1)
+    for low, high in ((0.1, 1.0), (-1.0, 1.0)):
+        x, f, b = conv_ref.conv_inputs(batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz,
+                                       f"fcb:{row}:{batch}:{low}", low=low, high=high)
+        got = _run_device(g, x, f, b, "conv_fc_stream", p)
+        if low > 0:
+            r = conv_ref.compare(got, conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True),
+                                 conv_ref.tolerance_for(op.in_chans * op.ksz ** 2))
+            assert r.ok, r
+        else:
+            pre = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=False).astype(np.float64)
+            bound = 1e-5 * conv_ref.signed_bound(x, f, op.stride, op.pad) + 1e-6
+            assert (np.abs(got.astype(np.float64) - np.maximum(pre, 0.0)) <= bound).all()
+            assert (got[pre < -bound] == 0.0).all() and (pre < -bound).any()
+            again = _run_device(g, x, f, b, "conv_fc_stream", p)
+            assert np.array_equal(got, again)
+
+
 @pytest.mark.parametrize("row,batch", [(0, 2), (29, 1), (31, 3), (39, 2), (41, 1)])
 def test_direct_nchw_kxk_full_size(cuda, row, batch):
     """tm=4: k x k stride-1 convs read straight from NCHW by 4-D TMA boxes whose x start is

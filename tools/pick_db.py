@@ -40,7 +40,9 @@ def main():
     ap.add_argument("--slack", type=float, default=1.0)
     a = ap.parse_args()
     by = defaultdict(list)
-    with open(a.cands) as fh:
+    import gzip
+
+    with (gzip.open(a.cands, "rt") if a.cands.endswith(".gz") else open(a.cands)) as fh:
         for r in csv.DictReader(fh):
             by[r["signature"]].append((float(r["ns"]), int(r["ctas"]), r["variant"], r["params"]))
     db = tuner.TuneDB()
