@@ -48,6 +48,15 @@ CASES = [
     ("k_tconv bf16 1x1 NCHW", (2, 64, 12, 12), (1, 1, 0, 64), "conv_1x1", P + "BN=64,sk=1,sw=0,dr=0,tm=3,pr=1"),
     ("k_fc_stream", (2, 16, 4, 4), (4, 1, 0, 64), "conv_fc_stream", "MNt=1:4,MNb=4:1,Kb=1,vw=1,lf=1,li=1"),
     ("k_fc_smem", (3, 16, 4, 4), (4, 1, 0, 64), "conv_fc_stream", "MNt=1:2,MNb=4:1,Kb=2,vw=1,lf=1,li=1"),
+    ("k_fc_bulk", (3, 16, 8, 8), (8, 1, 0, 72), "conv_fc_stream", "MNt=1:1,MNb=8:1,Kb=3,vw=1,lf=1,li=1"),
+    ("k_tconv MODE0 2-SM pair", (2, 32, 12, 12), (3, 1, 1, 128), "conv_umma", P + "BN=128,sk=1,sw=0,dr=0,tm=1,cl=3"),
+    ("k_tconv MODE0 2-SM pair stream-K", (2, 32, 12, 12), (3, 1, 1, 96), "conv_umma", P + "BN=96,sk=0,sw=0,dr=0,tm=1,cl=3"),
+    ("k_tconv split-K cluster", (1, 64, 12, 12), (3, 1, 1, 64), "conv_umma", P + "BN=64,sk=2,sw=0,dr=0,tm=1,cl=4"),
+    ("k_tconv first-layer space-to-depth", (1, 3, 35, 35), (11, 4, 0, 32), "conv_umma", P + "BN=32,sk=1,sw=0,dr=0,tm=6"),
+    ("k_tconv bf16 SS", (2, 64, 12, 12), (3, 1, 1, 128), "conv_umma", P + "BN=128,sk=1,sw=0,dr=0,tm=5,pr=1"),
+    ("k_tconv bf16 SS pair", (2, 64, 12, 12), (3, 1, 1, 128), "conv_umma", P + "BN=128,sk=1,sw=0,dr=0,tm=5,cl=3,pr=1"),
+    ("k_tconv fp8", (2, 64, 12, 12), (3, 1, 1, 64), "conv_umma", P + "BN=64,sk=1,sw=0,dr=0,tm=1,pr=2"),
+    ("k_wino + MODE7", (2, 32, 12, 12), (3, 1, 1, 64), "conv_wino", P + "BN=64,sk=1,sw=0,dr=0"),
 ]
 
 
@@ -77,7 +86,7 @@ def main():
         ref = runner.ConvOp(VARIANTS["conv_simple"].generate(node, g.edges, TuneParams()), x, w, b)
         ref.launch()
         torch.cuda.synchronize()
-        k = 8e-3 if params.prec else 1e-5
+        k = {0: 1e-5, 1: 8e-3, 2: 0.14}[params.prec]  # the modes' stated signed bounds (fp8: per-product e4m3)
         # sum|x||w| per output by the exact-order kernel itself (no library conv in a sanitizer run)
         gb = graph(dims, kp, relu=False)
         absop = runner.ConvOp(VARIANTS["conv_simple"].generate(gb.node("conv"), gb.edges, TuneParams()), x.abs(),
