@@ -1087,14 +1087,15 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     }
                     if (Cfg::PAIR) {  // both CTAs' stage, A slot and accumulator slot
                         tc_commit_pair(smem_u32(&empty_bar[stage]), (uint16_t)0x3);
-                        tc_commit_pair(smem_u32(&afree_bar[n % Cfg::A_SLOTS]), (uint16_t)0x3);
+                        if (!Cfg::SS)  // (SS: no A slots in TMEM, nobody waits on afree)
+                            tc_commit_pair(smem_u32(&afree_bar[n % Cfg::A_SLOTS]), (uint16_t)0x3);
                         if (last) tc_commit_pair(smem_u32(&tfull_bar[slot]), (uint16_t)0x3);
                     } else {
                     if (CL == 2)  // the stage's filter half may be refilled by either CTA
                         tc_commit_mc(smem_u32(&empty_bar[stage]), (uint16_t)0x3);
                     else
                         tc_commit(smem_u32(&empty_bar[stage]));
-                    tc_commit(smem_u32(&afree_bar[n % Cfg::A_SLOTS]));
+                    if (!Cfg::SS) tc_commit(smem_u32(&afree_bar[n % Cfg::A_SLOTS]));
                     if (last) tc_commit(smem_u32(&tfull_bar[slot]));
                     }
                     if (n < 32) B2C_TRACE(a.trace, 144 + n);
