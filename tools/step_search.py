@@ -1,0 +1,169 @@
+#!/usr/bin/env python
+"""Re-pick the sweep DB against the concurrent step itself (GPU box).
+
+tools/pick_db.py chooses, per op, a candidate by a proxy (isolated cold time x
+SM share); what the bench's step measures is the ops running side by side on 16
+graph branches.  This search starts from a sweep DB and, op by op in order of
+the SM-time they hold, tries the best few alternative candidates of that op
+(the tuner's full candidate table, all already validated on the device) inside
+the real concurrent step: capture the step graph with the alternative, time it
+interleaved with the incumbent (CUDA events, min of several replay batches),
+keep the alternative only if the step gets faster by more than --min-gain.
+
+    python tools/step_search.py --cands cands_fp32.csv.gz --db data/tunedb_b200_fp32_sweep.tsv \
+        --out gpurun_out/sweep_searched.tsv [--prec 0] [--alts 3] [--passes 1]
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import gzip
+import os
+import sys
+import time
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1611_06945_b200 import runner, tuner  # noqa: E402
+from paper_1611_06945_b200.backend import CostReport  # noqa: E402
+from paper_1611_06945_b200.variants import VARIANTS, TuneParams  # noqa: E402
+
+SMS = 148
+
+
+def load_cands(path):
+    by = defaultdict(list)
+    with (gzip.open(path, "rt") if path.endswith(".gz") else open(path)) as fh:
+        for r in csv.DictReader(fh):
+            by[r["signature"]].append((float(r["ns"]), int(r["ctas"]), r["variant"], r["params"]))
+    return by
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cands", required=True)
+    ap.add_argument("--db", required=True, help="starting sweep DB")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--prec", type=int, default=0)
+    ap.add_argument("--alts", type=int, default=3, help="alternatives tried per op")
+    ap.add_argument("--slack", type=float, default=3.0, help="only candidates within slack x the op's fastest")
+    ap.add_argument("--passes", type=int, default=1)
+    ap.add_argument("--streams", type=int, default=16)
+    ap.add_argument("--reps", type=int, default=20, help="step replays per timing batch")
+    ap.add_argument("--batches", type=int, default=3, help="timing batches per measurement (min taken)")
+    ap.add_argument("--min-gain", type=float, default=0.004, help="relative step-time gain needed to switch")
+    a = ap.parse_args()
+
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    cands = load_cands(a.cands)
+    db = tuner.load_db(a.db)
+    sweep = bench.build_sweep((1, 5, 20), db, False, prec=a.prec)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(a.streams)]
+
+    units = []  # per sweep unit: dict(sig, node, edges, x, w, b, cur=(vname, ps, ns, ctas), op=ConvOp)
+    for row, op, node, edges, v, params in sweep:
+        sig = tuner.op_signature(node, edges)
+        x, f, b = bench.make_inputs(op, node, edges)
+        dx, df, db_ = (torch.from_numpy(t.copy()).to(dev) for t in (x, f, b))
+        rec = db.records[sig]
+        cur = next((c for c in cands.get(sig, []) if c[2] == rec.variant and c[3] == rec.params.to_string()),
+                   (rec.cost, SMS, rec.variant, rec.params.to_string()))
+        u = {"sig": sig, "row": row, "n": op.batch, "node": node, "edges": edges, "x": dx, "w": df, "b": db_,
+             "cur": cur}
+        u["op"] = make_op(u, cur)
+        units.append(u)
+    torch.cuda.synchronize()
+
+    def step_ms(ops_est):
+        g = bench.capture(ops_est, streams)
+        s0 = streams[0]
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(a.batches):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s0):
+                e0.record(s0)
+                for _ in range(a.reps):
+                    g.replay()
+                e1.record(s0)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / a.reps)
+        del g
+        return best
+
+    def current():
+        return [(u["op"], u["cur"][0] * 1e-6) for u in units]
+
+    base = step_ms(current())
+    print(f"start: {base * 1e3:.1f} us per step", flush=True)
+    t0 = time.time()
+    changed = 0
+    for p in range(a.passes):
+        order = sorted(range(len(units)), key=lambda i: -units[i]["cur"][0] * min(units[i]["cur"][1], SMS))
+        for i in order:
+            u = units[i]
+            pool = cands.get(u["sig"], [])
+            if not pool:
+                continue
+            fastest = min(c[0] for c in pool)
+            alts = [c for c in pool if c[0] <= a.slack * fastest and (c[2], c[3]) != (u["cur"][2], u["cur"][3])]
+            alts.sort(key=lambda c: c[0] * (min(c[1], SMS) / SMS) ** 0.5)
+            seen, tried = set(), 0
+            for c in alts:
+                if tried >= a.alts or (c[2], c[3]) in seen:
+                    continue
+                seen.add((c[2], c[3]))
+                tried += 1
+                try:
+                    alt_op = make_op(u, c)
+                except Exception as e:  # an inapplicable / failing candidate: skip it
+                    print(f"  row{u['row']} N={u['n']} {c[3]}: skipped ({type(e).__name__})", flush=True)
+                    continue
+                ops = current()
+                ops[i] = (alt_op, c[0] * 1e-6)
+                t_alt = step_ms(ops)
+                t_cur = step_ms(current())  # interleaved re-measure of the incumbent
+                base = min(base, t_cur)
+                if t_alt < min(t_cur, base) * (1.0 - a.min_gain):
+                    t_alt2 = step_ms(ops)  # confirm
+                    if t_alt2 < min(t_cur, base) * (1.0 - a.min_gain / 2):
+                        print(f"  row{u['row']:2d} N={u['n']:2d} {u['cur'][2]}:{u['cur'][3].split('li=1,')[-1]} -> "
+                              f"{c[2]}:{c[3].split('li=1,')[-1]}  step {t_cur * 1e3:.1f} -> {min(t_alt, t_alt2) * 1e3:.1f} us",
+                              flush=True)
+                        u["op"], u["cur"] = alt_op, c
+                        base = min(t_alt, t_alt2)
+                        changed += 1
+                        continue
+                del alt_op
+        print(f"pass {p}: {changed} changes, step {base * 1e3:.1f} us ({time.time() - t0:.0f}s)", flush=True)
+
+    out = tuner.TuneDB()
+    for sig, rec in db.records.items():
+        out.add(rec)
+    for u in units:
+        ns, ctas, vname, ps = u["cur"]
+        out.add(tuner.TuneRecord(u["sig"], vname, TuneParams.from_string(ps), ns, CostReport(wall_ns=int(ns)),
+                                 objective=tuner.WALL))
+    tuner.save_db(out, a.out)
+    final = step_ms(current())
+    print(f"final: {final * 1e3:.1f} us per step, {changed} ops changed -> {a.out}", flush=True)
+
+
+def make_op(u, c):
+    ns, ctas, vname, ps = c
+    v = VARIANTS[vname]
+    plan = v.generate(u["node"], u["edges"], TuneParams.from_string(ps))
+    return runner.ConvOp(plan, u["x"], u["w"], u["b"])
+
+
+if __name__ == "__main__":
+    main()
