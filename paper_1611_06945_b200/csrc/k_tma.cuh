@@ -79,6 +79,9 @@ constexpr int TM_SPLIT_THREADS = 128;  // warps 0-3
 constexpr int TM_HDR = 2048;           // barriers, TMEM slot, flags (< 1 KB); unit bias at +1 KB (<= 256 floats)
 constexpr int TM_MAX_SMEM = 232448;    // 227 KB opt-in per CTA
 constexpr int TM_TAPS = 8;             // MODE 3: filter taps per K block
+#ifndef B2C_FUSED_ON
+#define B2C_FUSED_ON 1
+#endif
 
 // PREC 0: fp32-exact 3xTF32 (kind::tf32, A = raw | lo in TMEM, B = packed raw | lo).
 // PREC 2: e4m3 operands, fp32 accumulate (kind::f8f6f4): as PREC 1 with one K = 32 MMA per
@@ -134,20 +137,29 @@ struct TmaCfg {
                                                                  : (SWAP ? 1 : 2) * FLT_ROWS * 128;  // packed filters per K block
     static constexpr int FLT_HALF = FLT_ROWS / 2 * 128;   // 2-SM pair: one CTA's rows of one (raw | lo) image
     static constexpr int FLT_CTA = PAIR ? (SS ? FLT_HALF : 2 * FLT_HALF) : FLT_STAGE;  // filter bytes landing in one CTA per K block
-    static constexpr int ACC_COLS = 2 * BN;               // two TMEM accumulation slots
+    static constexpr bool SW128 = MODE != 3;
+    // Fused 3xTF32 issue (PREC 0, B raw | lo contiguous in one SWIZZLE_128B image): the raw and
+    // lo B tiles form one N = 2*BN operand, so Ahi*[Braw | Blo] is ONE MMA and Alo*Braw a second
+    // one accumulating into the Blo half: 2 tcgen05.mma per K = 8 step instead of 3 (fewer
+    // issue slots for the single MMA-issuing thread).  An accumulator slot is then 2*BN columns
+    // [Ahi*Braw | Ahi*Blo + Alo*Braw], summed by the drain; kept where >= 2 A slots still fit.
+    static constexpr int TMEM_COLS0 = OCC == 2 ? 256 : 512;
+    static constexpr bool FUSED = B2C_FUSED_ON && PREC == 0 && !SS && !PAIR && SW128 && OCC == 1 && 2 * BN <= 256 &&
+                                  4 * BN + 128 <= TMEM_COLS0;
+    static constexpr int SLOT_COLS = FUSED ? 2 * BN : BN;  // TMEM columns per accumulation slot
+    static constexpr int ACC_COLS = 2 * SLOT_COLS;        // two TMEM accumulation slots
     // OCC CTAs per SM share its 228 KB of shared memory (1 KB per CTA is the driver's) and 512 TMEM columns
     static constexpr int BUDGET = (OCC == 1 ? TM_MAX_SMEM : 233472 / OCC - 1024) - TM_HDR - 1024 - STG_BYTES;
     static constexpr int SM_STAGES = BUDGET / STAGE_BYTES;
     static constexpr int STAGES = SM_STAGES < 8 ? SM_STAGES : 8;
     static constexpr int SMEM = TM_HDR + 1024 + STAGES * STAGE_BYTES + STG_BYTES;
-    static constexpr int TMEM_COLS = OCC == 2 ? 256 : 512;
+    static constexpr int TMEM_COLS = TMEM_COLS0;
     // TMEM A stages (raw | lo: 64 columns each): as many as the columns left beside the two
     // accumulators allow (<= 4), so a split is not held up waiting for the MMAs of the stage
     // two back to release its slot (the 2-slot loop was paced split -> MMA issue -> MMA done).
     static constexpr int A_SLOTS_FIT = (TMEM_COLS - ACC_COLS) / 64;
     static constexpr int A_SLOTS = A_SLOTS_FIT < 4 ? A_SLOTS_FIT : 4;
     static_assert(ACC_COLS + A_SLOTS * 64 <= TMEM_COLS, "TMEM budget");
-    static constexpr bool SW128 = MODE != 3;
     static constexpr uint32_t BYTES = PIX_ROWS * 128 + (RAW_B ? FLT_ROWS * 128 : FLT_CTA);
     static constexpr uint32_t FLT_BYTES = RAW_B ? FLT_ROWS * 128 : FLT_CTA;  // the filter warp's bytes per stage
     // barrier arrival counts (a pair's leader counts its peer's split / drain warps too)
@@ -981,7 +993,8 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                 const int slot = cidx & 1;
                 mbar_wait(smem_u32(&tfull_bar[slot]), (uint32_t)(cidx >> 1) & 1u);
                 tc_fence_after();
-                tmem_add_cols<DC>(t_row + (uint32_t)(slot * BN), acc);
+                tmem_add_cols<DC>(t_row + (uint32_t)(slot * Cfg::SLOT_COLS), acc);
+                if (Cfg::FUSED) tmem_add_cols<DC>(t_row + (uint32_t)(slot * Cfg::SLOT_COLS + BN), acc);
                 tc_fence_before();
                 if (Cfg::PAIR) {
                     __syncwarp();
@@ -1036,7 +1049,7 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                     const uint32_t a_lo = a_hi + 32;
                     const uint32_t b_raw = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::A_SMEM);
                     const uint32_t b_lo = b_raw + (Cfg::PAIR ? BN / 2 : BN) * 128;
-                    const uint32_t d = tmem_base + (uint32_t)(slot * BN);
+                    const uint32_t d = tmem_base + (uint32_t)(slot * Cfg::SLOT_COLS);
                     if constexpr (Cfg::SS) {  // bf16 SS: four K = 16 MMAs per 64-wide K block, +32 B per step
                         const uint32_t a_s = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES + Cfg::PIX_OFF);
 #pragma unroll
@@ -1070,7 +1083,11 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
                             dbh = umma_desc(b_raw + s * 2 * BN * 16, BN * 16, 128);
                             dbl = umma_desc(b_lo + s * 2 * BN * 16, BN * 16, 128);
                         }
-                        if constexpr (Cfg::PAIR) {
+                        if constexpr (Cfg::FUSED) {  // [d, d+2BN) = Ahi*[Braw | Blo]; [d+BN, d+2BN) += Alo*Braw
+                            constexpr uint32_t idesc2 = umma_idesc(2, TM_M, 2 * BN);
+                            mma_tf32_ts(d, a_hi + 8 * s, dbh, idesc2, (first && s == 0) ? 0u : 1u);
+                            mma_tf32_ts(d + BN, a_lo + 8 * s, dbh, idesc, 1u);
+                        } else if constexpr (Cfg::PAIR) {
                             mma_tf32_ts_pair(d, a_hi + 8 * s, dbh, idesc, (first && s == 0) ? 0u : 1u);
                             if (!(a.trace & 2)) {
                                 mma_tf32_ts_pair(d, a_hi + 8 * s, dbl, idesc, 1u);
