@@ -854,6 +854,27 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     const int rank = CL >= 2 ? (int)cluster_ctarank() : 0;
     constexpr int NCTA = Cfg::TWO_TILES ? 2 : 1;  // CTAs walking one unit sequence
     const int ubase = (int)blockIdx.x / NCTA, ustride = (int)gridDim.x / NCTA;
+    // The loaders decode their first unit before the set-up barrier: it reads only kernel
+    // parameters, and their first-touch constant-cache misses (~800 cycles, profiles/r2be)
+    // then overlap barrier init / TMEM allocation instead of delaying the first TMA.
+    UnitCursor ld_cur{};
+    Unit ld_w{};
+    bool ld_first = false;
+    if ((warp == Cfg::LOAD_WARP || warp == Cfg::FLT_WARP) && lane == 0) {
+        ld_cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
+        ld_first = next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ld_cur, ustride, rank, ld_w);
+        // touch the rest of the parameter block the loaders' loops read (one field per 64 B): the
+        // constant-cache lines are then resident when the loops start after griddepcontrol.wait
+        const uint32_t sink = (uint32_t)g.OW + g.fPQ.mul + g.fOW.mul + g.fR.mul + (uint32_t)(size_t)a.wpk +
+                              (uint32_t)a.kblocks + (uint32_t)a.bx + (uint32_t)a.by + a.fCB.mul + (uint32_t)a.drain +
+                              (uint32_t)a.hp + (uint32_t)a.box_w + (uint32_t)a.kb_period + a.fTilesX.mul + (uint32_t)a.trace;
+        asm volatile("" ::"r"(sink));
+    }
+    // the flags every warp branches on right after griddepcontrol.wait, read here for the same reason
+    // (asm volatile pins the reads to this point)
+    int relayout_on, flt_early_on;
+    asm volatile("mov.b32 %0, %1;" : "=r"(relayout_on) : "r"(a.relayout));
+    asm volatile("mov.b32 %0, %1;" : "=r"(flt_early_on) : "r"(a.flt_early));
     if (tid == 0) B2C_TRACE(a.trace, 0);
 
     if (tid == 0) {
@@ -893,12 +914,150 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
     // The loader may stream the first stages' packed filters (constant, written
     // by an earlier synchronised b2c_conv_prepare) while the previous kernel
     // (the x re-layout) is still running; everything else waits for it here.
-    const bool early = Cfg::TWO_LOADERS && a.flt_early && !Cfg::RAW_B && !a.relayout && warp == Cfg::FLT_WARP;
+    const bool early = Cfg::TWO_LOADERS && flt_early_on && !Cfg::RAW_B && !relayout_on && warp == Cfg::FLT_WARP;
     if (!early) pdl_wait();
-    if (a.relayout) fused_relayout(a, smem + TM_HDR + 1024);
+    if (warp == Cfg::LOAD_WARP && lane == 0) B2C_TRACE(a.trace, 14);
+    if (relayout_on) fused_relayout(a, smem + TM_HDR + 1024);
     if (tid == 0) B2C_TRACE(a.trace, 3);
 
-    if (warp < 4) {
+    // the loaders first: their code then follows the prologue in the binary (their first TMA is on the
+    // critical path of every launch; the other roles wait on barriers behind it)
+    if (warp == Cfg::LOAD_WARP && lane == 0) {
+        // ------------------------------------------------------------ pixel / activation loader (TMA)
+        // (with one loader warp, OCC == 2, it issues each stage's filters too; the early filter
+        // prefetch is then off)
+        int stage = 0, n = 0;
+        uint32_t phase = 0;
+        B2C_TRACE(a.trace, 10);
+        UnitCursor cur = ld_cur;
+        Unit w = ld_w;
+        for (bool have = ld_first; have; have = next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w)) {
+            if (n == 0) B2C_TRACE(a.trace, 11);
+            int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
+            if (MODE == 0 || MODE == 3 || MODE == 8) {
+                uint32_t b, p, oy, ox;
+                g.fPQ.divmod((uint32_t)w.m0, b, p);
+                g.fOW.divmod(p, oy, ox);
+                pw = (int)ox * g.S - g.P;
+                ph = (int)oy * g.S - g.P;
+                pn = (int)b;
+            }
+            for (int i = 0; i < w.nkb; ++i, ++n) {
+                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
+                if (n == 0) B2C_TRACE(a.trace, 12);
+                const uint32_t bar = smem_u32(&raw_full[stage]);
+                const uint32_t pix = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::PIX_OFF;
+                const int kb = w.kb_begin + i;
+                // MODE 4 / 6 boxes are bx*by / box_w*by rows (<= 128): the rest of the tile keeps
+                // stale (finite) data whose output rows the epilogue discards.
+                const uint32_t bytes = (MODE == 4   ? (uint32_t)(a.bx * a.by) * 128u
+                                        : MODE == 6 ? (uint32_t)(a.box_w * a.by) * 128u
+                                                    : (uint32_t)Cfg::PIX_ROWS * 128u) +
+                                       (Cfg::TWO_LOADERS ? 0u : Cfg::FLT_BYTES);
+                mbar_arrive_expect_tx(bar, bytes);
+                if (!Cfg::TWO_LOADERS) {
+                    const uint32_t dst = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::FLT_OFF;
+                    if (MODE == 1)
+                        tma_load_2d(dst, &tm_flt, bar, kb * TM_BK, w.n0);
+                    else if (MODE == 7)
+                        tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
+                    else
+                        load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(
+                            dst, reinterpret_cast<const char*>(a.wpk) +
+                                     ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + kb) * (size_t)Cfg::FLT_STAGE, bar, rank);
+                }
+                if (n < 32) B2C_TRACE(a.trace, 176 + n);
+                if (MODE == 1 || MODE == 2) {
+                    tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
+                } else if (MODE == 7) {  // V[z] rows: (k, row, z)
+                    tma_load_3d(pix, &tm_pix, bar, kb * TM_BK, w.m0, w.b);
+                } else if (MODE == 5) {  // (pixel run, channel block, image) straight from NCHW x
+                    tma_load_3d(pix, &tm_pix, bar, w.ox0, kb * TM_BK, w.b);
+                } else if (MODE == 6) {  // (x, y, channel block, image) of NCHW x; x start rounded down to 16 B
+                    uint32_t tap, cb, ky, kx;
+                    a.fCB.divmod((uint32_t)kb, tap, cb);
+                    g.fR.divmod(tap, ky, kx);
+                    const int dx = w.ox0 + (int)kx - g.P;
+                    const int xs = ((dx >= 0 ? dx : dx - 3) / 4) * 4;  // floor to a multiple of 4 floats
+                    tma_load_4d(pix, &tm_pix, bar, xs, w.oy0 + (int)ky - g.P, (int)cb * TM_BK, w.b);
+                } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
+                    uint32_t ky, kc;
+                    a.fCB.divmod((uint32_t)kb, ky, kc);
+                    tma_load_5d(pix, &tm_pix, bar, (int)kc * TM_BK, w.ox0, w.oy0, (int)ky, w.b);
+                } else if (MODE == 0 || MODE == 8) {  // MODE 8: 64 bf16 channels per block
+                    uint32_t tap, cb, ky, kx;
+                    a.fCB.divmod((uint32_t)kb, tap, cb);
+                    g.fR.divmod(tap, ky, kx);
+                    tma_load_im2col_4d(pix, &tm_pix, bar, (int)cb * (MODE == 8 ? 64 : TM_BK), pw, ph, pn, (uint16_t)kx,
+                                       (uint16_t)ky);
+                } else {  // MODE 3: 8 taps x 4 channels, one 16-byte-pixel box per tap
+#pragma unroll 1
+                    for (int j = 0; j < TM_TAPS; ++j) {
+                        const int tap = kb * TM_TAPS + j;
+                        uint32_t ky = 0, kx = 0;
+                        int c = 4;  // taps past R*R: channel 4 is out of bounds -> zeros
+                        if (tap < g.RR) {
+                            g.fR.divmod((uint32_t)tap, ky, kx);
+                            c = 0;
+                        }
+                        tma_load_im2col_4d(pix + (uint32_t)(j * Cfg::PIX_ROWS * 16), &tm_pix, bar, c, pw, ph, pn,
+                                           (uint16_t)kx, (uint16_t)ky);
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (Cfg::TWO_LOADERS && warp == Cfg::FLT_WARP && lane == 0) {
+        // ------------------------------------------------------------ filter loader (bulk copies / TMA)
+        int stage = 0, n = 0;
+        uint32_t phase = 0;
+        int npre = 0;  // stages whose filter bytes were issued before griddepcontrol.wait
+        if (early) {
+            if (ld_first) {
+                const Unit& w0 = ld_w;
+                npre = min(STAGES, w0.nkb);
+                const char* wsrc0 = reinterpret_cast<const char*>(a.wpk) +
+                                    ((size_t)(w0.n0 / Cfg::FLT_ROWS) * a.kblocks + w0.kb_begin) * (size_t)Cfg::FLT_STAGE;
+                for (int i = 0; i < npre; ++i) {  // fresh stages: no empty wait
+                    const uint32_t bar = smem_u32(&raw_full[i]);
+                    mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
+                    load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
+                                                    wsrc0 + (size_t)i * Cfg::FLT_STAGE, bar, rank);
+                }
+            }
+            B2C_TRACE(a.trace, 8);
+            pdl_wait();
+            B2C_TRACE(a.trace, 9);
+        }
+        UnitCursor cur = ld_cur;
+        Unit w = ld_w;
+        for (bool have = ld_first; have; have = next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w)) {
+            const char* wsrc = reinterpret_cast<const char*>(a.wpk) +
+                               ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + w.kb_begin) * (size_t)Cfg::FLT_STAGE;
+            for (int i = 0; i < w.nkb; ++i, ++n) {
+                if (n >= npre) {  // (stages issued early were armed and loaded above)
+                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
+                    const uint32_t bar = smem_u32(&raw_full[stage]);
+                    const uint32_t dst = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::FLT_OFF;
+                    const int kb = w.kb_begin + i;
+                    mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
+                    if (MODE == 1)
+                        tma_load_2d(dst, &tm_flt, bar, kb * TM_BK, w.n0);
+                    else if (MODE == 7)  // U[z] rows: (k, row, z)
+                        tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
+                    else
+                        load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(dst, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp < 4) {
         // ------------------------------------------------------------ split: A -> TMEM (raw | lo), B lo -> smem
         if constexpr (Cfg::SS && Cfg::PAIR) {  // SS pair: forward this CTA's stage-full to the leader's MMA warp
             if (warp == 0 && lane == 0) {
@@ -1131,137 +1290,6 @@ __global__ void __launch_bounds__(TmaCfg<BN, SWAP, MODE, OCC, CL, PREC>::THREADS
             }
         }
         if (lane == 0) B2C_TRACE(a.trace, 5);
-    } else if (warp == Cfg::LOAD_WARP && lane == 0) {
-        // ------------------------------------------------------------ pixel / activation loader (TMA)
-        // (with one loader warp, OCC == 2, it issues each stage's filters too; the early filter
-        // prefetch is then off)
-        int stage = 0, n = 0;
-        uint32_t phase = 0;
-        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
-        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
-            int pw = 0, ph = 0, pn = 0;  // im2col base of the unit's first pixel
-            if (MODE == 0 || MODE == 3 || MODE == 8) {
-                uint32_t b, p, oy, ox;
-                g.fPQ.divmod((uint32_t)w.m0, b, p);
-                g.fOW.divmod(p, oy, ox);
-                pw = (int)ox * g.S - g.P;
-                ph = (int)oy * g.S - g.P;
-                pn = (int)b;
-            }
-            for (int i = 0; i < w.nkb; ++i, ++n) {
-                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
-                const uint32_t bar = smem_u32(&raw_full[stage]);
-                const uint32_t pix = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::PIX_OFF;
-                const int kb = w.kb_begin + i;
-                // MODE 4 / 6 boxes are bx*by / box_w*by rows (<= 128): the rest of the tile keeps
-                // stale (finite) data whose output rows the epilogue discards.
-                const uint32_t bytes = (MODE == 4   ? (uint32_t)(a.bx * a.by) * 128u
-                                        : MODE == 6 ? (uint32_t)(a.box_w * a.by) * 128u
-                                                    : (uint32_t)Cfg::PIX_ROWS * 128u) +
-                                       (Cfg::TWO_LOADERS ? 0u : Cfg::FLT_BYTES);
-                mbar_arrive_expect_tx(bar, bytes);
-                if (!Cfg::TWO_LOADERS) {
-                    const uint32_t dst = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::FLT_OFF;
-                    if (MODE == 1)
-                        tma_load_2d(dst, &tm_flt, bar, kb * TM_BK, w.n0);
-                    else if (MODE == 7)
-                        tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
-                    else
-                        load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(
-                            dst, reinterpret_cast<const char*>(a.wpk) +
-                                     ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + kb) * (size_t)Cfg::FLT_STAGE, bar, rank);
-                }
-                if (n < 32) B2C_TRACE(a.trace, 176 + n);
-                if (MODE == 1 || MODE == 2) {
-                    tma_load_2d(pix, &tm_pix, bar, kb * TM_BK, w.m0);
-                } else if (MODE == 7) {  // V[z] rows: (k, row, z)
-                    tma_load_3d(pix, &tm_pix, bar, kb * TM_BK, w.m0, w.b);
-                } else if (MODE == 5) {  // (pixel run, channel block, image) straight from NCHW x
-                    tma_load_3d(pix, &tm_pix, bar, w.ox0, kb * TM_BK, w.b);
-                } else if (MODE == 6) {  // (x, y, channel block, image) of NCHW x; x start rounded down to 16 B
-                    uint32_t tap, cb, ky, kx;
-                    a.fCB.divmod((uint32_t)kb, tap, cb);
-                    g.fR.divmod(tap, ky, kx);
-                    const int dx = w.ox0 + (int)kx - g.P;
-                    const int xs = ((dx >= 0 ? dx : dx - 3) / 4) * 4;  // floor to a multiple of 4 floats
-                    tma_load_4d(pix, &tm_pix, bar, xs, w.oy0 + (int)ky - g.P, (int)cb * TM_BK, w.b);
-                } else if (MODE == 4) {  // (window chunk, ox, oy, ky, image)
-                    uint32_t ky, kc;
-                    a.fCB.divmod((uint32_t)kb, ky, kc);
-                    tma_load_5d(pix, &tm_pix, bar, (int)kc * TM_BK, w.ox0, w.oy0, (int)ky, w.b);
-                } else if (MODE == 0 || MODE == 8) {  // MODE 8: 64 bf16 channels per block
-                    uint32_t tap, cb, ky, kx;
-                    a.fCB.divmod((uint32_t)kb, tap, cb);
-                    g.fR.divmod(tap, ky, kx);
-                    tma_load_im2col_4d(pix, &tm_pix, bar, (int)cb * (MODE == 8 ? 64 : TM_BK), pw, ph, pn, (uint16_t)kx,
-                                       (uint16_t)ky);
-                } else {  // MODE 3: 8 taps x 4 channels, one 16-byte-pixel box per tap
-#pragma unroll 1
-                    for (int j = 0; j < TM_TAPS; ++j) {
-                        const int tap = kb * TM_TAPS + j;
-                        uint32_t ky = 0, kx = 0;
-                        int c = 4;  // taps past R*R: channel 4 is out of bounds -> zeros
-                        if (tap < g.RR) {
-                            g.fR.divmod((uint32_t)tap, ky, kx);
-                            c = 0;
-                        }
-                        tma_load_im2col_4d(pix + (uint32_t)(j * Cfg::PIX_ROWS * 16), &tm_pix, bar, c, pw, ph, pn,
-                                           (uint16_t)kx, (uint16_t)ky);
-                    }
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-            }
-        }
-    } else if (Cfg::TWO_LOADERS && warp == Cfg::FLT_WARP && lane == 0) {
-        // ------------------------------------------------------------ filter loader (bulk copies / TMA)
-        int stage = 0, n = 0;
-        uint32_t phase = 0;
-        int npre = 0;  // stages whose filter bytes were issued before griddepcontrol.wait
-        if (early) {
-            UnitCursor c0 = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
-            Unit w0;
-            if (next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, c0, ustride, rank, w0)) {
-                npre = min(STAGES, w0.nkb);
-                const char* wsrc0 = reinterpret_cast<const char*>(a.wpk) +
-                                    ((size_t)(w0.n0 / Cfg::FLT_ROWS) * a.kblocks + w0.kb_begin) * (size_t)Cfg::FLT_STAGE;
-                for (int i = 0; i < npre; ++i) {  // fresh stages: no empty wait
-                    const uint32_t bar = smem_u32(&raw_full[i]);
-                    mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
-                    load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(tiles_u32 + (uint32_t)(i * Cfg::STAGE_BYTES) + Cfg::FLT_OFF,
-                                                    wsrc0 + (size_t)i * Cfg::FLT_STAGE, bar, rank);
-                }
-            }
-            B2C_TRACE(a.trace, 8);
-            pdl_wait();
-            B2C_TRACE(a.trace, 9);
-        }
-        UnitCursor cur = cursor_begin<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, ubase);
-        for (Unit w; next_unit<Cfg::PIX_ROWS, Cfg::FLT_ROWS, MODE, CL>(a, cur, ustride, rank, w);) {
-            const char* wsrc = reinterpret_cast<const char*>(a.wpk) +
-                               ((size_t)(w.n0 / Cfg::FLT_ROWS) * a.kblocks + w.kb_begin) * (size_t)Cfg::FLT_STAGE;
-            for (int i = 0; i < w.nkb; ++i, ++n) {
-                if (n >= npre) {  // (stages issued early were armed and loaded above)
-                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
-                    const uint32_t bar = smem_u32(&raw_full[stage]);
-                    const uint32_t dst = tiles_u32 + (uint32_t)(stage * Cfg::STAGE_BYTES) + Cfg::FLT_OFF;
-                    const int kb = w.kb_begin + i;
-                    mbar_arrive_expect_tx(bar, Cfg::FLT_BYTES);
-                    if (MODE == 1)
-                        tma_load_2d(dst, &tm_flt, bar, kb * TM_BK, w.n0);
-                    else if (MODE == 7)  // U[z] rows: (k, row, z)
-                        tma_load_3d(dst, &tm_flt, bar, kb * TM_BK, w.n0, w.b);
-                    else
-                        load_filters<Cfg::FLT_STAGE, CL, Cfg::SS>(dst, wsrc + (size_t)i * Cfg::FLT_STAGE, bar, rank);
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-            }
-        }
     }
     if (tid == 0) B2C_TRACE(a.trace, 2);
     __syncthreads();

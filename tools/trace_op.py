@@ -42,7 +42,7 @@ for rep in range(2):
     torch.cuda.synchronize()
     L.b2c_debug_trace_read(buf)
     t0 = buf[0]
-    names = {0: "entry", 1: "setup", 2: "split_end", 3: "tid0_pdl", 4: "drains_done", 5: "mma_last_commit", 6: "epi_done", 7: "exit", 8: "ld_early", 9: "ld_pdl", 10: "ld2_top", 11: "ld2_empty", 12: "ld2_expect", 13: "ld2_pixtma", 14: "ld2_flt"}
+    names = {0: "entry", 1: "setup", 2: "split_end", 3: "tid0_pdl", 4: "drains_done", 5: "mma_last_commit", 6: "epi_done", 7: "exit", 8: "ld_early", 9: "ld_pdl", 10: "ld2_top", 11: "ld2_empty", 12: "ld2_expect", 13: "ld2_pixtma", 14: "ld_after_wait"}
     print(f"--- row{a.row} N={a.batch} {p.to_string()} rep{rep} (clk rel. entry)")
     print("  " + "  ".join(f"{names[i]}={buf[i] - t0}" for i in sorted(names) if buf[i]))
     def row(name, base):
