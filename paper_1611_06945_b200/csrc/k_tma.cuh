@@ -724,17 +724,19 @@ __device__ __forceinline__ void epilogue_unit(const TArgs& a, const Unit& w, flo
         float* part = a.ws + ((size_t)w.pslot0 + w.z) * BN * TM_M;
 #pragma unroll
         for (int j = 0; j < DC; ++j) __stcg(part + (size_t)(c_begin + j) * TM_M + row, acc[j]);
-        __threadfence();
+        // Ordering without a per-thread SC fence: the barrier orders this CTA's partial stores
+        // before the ticket, and the ticket is an acq_rel atomic at gpu scope (its release is
+        // cumulative over the barrier; its acquire, by the last contributor, makes every other
+        // contributor's partials visible to this CTA's cache-global loads after the next barrier).
         named_bar_sync(1, NT);
         if (dtid == 0) {
-            const int ticket = atomicAdd(a.sems + w.t, 1);
+            const int ticket = atom_add_acq_rel_gpu(a.sems + w.t, 1);
             *last_flag = (ticket == w.nsplit - 1);
         }
         named_bar_sync(1, NT);
         const bool last = *last_flag != 0;
         named_bar_sync(1, NT);  // last_flag is rewritten by the next unit
         if (!last) return;
-        __threadfence();
         if (dtid == 0) a.sems[w.t] = 0;
 #pragma unroll
         for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
