@@ -700,6 +700,10 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
     e2e = None
     if hosts or (world > 1 and not args.no_e2e):
         side = [torch.cuda.Stream(device=dev) for _ in range(E2E_STREAMS)]
+        # the ops are independent: interleave the most input-heavy with the most output-heavy ones
+        # so that the H2D and D2H copy engines stay busy together (profiles/r2am/e2e_probe.log)
+        by_ratio = sorted(hosts, key=lambda h: h.d2h_bytes / max(1, h.h2d_bytes))
+        e2e_order = [by_ratio[(j // 2) if j % 2 == 0 else len(by_ratio) - 1 - j // 2] for j in range(len(by_ratio))]
         for h in hosts:
             h.run(main.cuda_stream)
         torch.cuda.synchronize()
@@ -712,7 +716,7 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
             for s in side:
                 s.wait_event(e0)
             for _ in range(ksteps):
-                for i, h in enumerate(hosts):
+                for i, h in enumerate(e2e_order):
                     h.run(side[i % E2E_STREAMS].cuda_stream)
             for s in side:
                 main.wait_stream(s)
@@ -733,7 +737,7 @@ def run_ours(args, rank, world, local_rank, one_gpu_test=False):
                "pcie_measured": pcie, "copy_bound_ms": round(copy_ms, 3),
                "frac_of_copy_bound": round(copy_ms / e_ms, 4),
                "path": f"b2c_conv_fwd_host per op (pinned H2D x/w/bias + filter pack + kernel + D2H y), "
-                       f"ops round-robin on {E2E_STREAMS} streams" + (" (bytes: rank 0's share)" if world > 1 else "")}
+                       f"ops round-robin on {E2E_STREAMS} streams, input-heavy and output-heavy ops interleaved" + (" (bytes: rank 0's share)" if world > 1 else "")}
 
     if rank != 0:
         return
