@@ -105,8 +105,8 @@ def test_slabs_gathered_to_root_bit_identical(cuda):
 def test_bench_two_ranks_shard_mode_control_flow(cuda):
     env = dict(os.environ, B2C_BENCH_ONE_GPU_TEST="1")
     env.pop("WORLD_SIZE", None)
-    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "1",
-           "--no-cpu", "--no-e2e"]
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--no-cpu"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
@@ -115,3 +115,4 @@ def test_bench_two_ranks_shard_mode_control_flow(cuda):
     assert mg["gather"] and mg["gather_inclusive_ms"] >= mg["compute_only_ms"] > 0
     assert line["config"]["flops_per_step"] == 152691710080  # the whole sweep, split over the ranks
     assert line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0  # host-buffer path on both ranks
