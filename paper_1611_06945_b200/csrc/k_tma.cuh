@@ -44,7 +44,8 @@
 //
 // Precision (see k_umma.cuh): kind::tf32 truncates an fp32 operand to TF32,
 // so raw x is the "hi" operand and lo = x - trunc_tf32(x);
-// D += Ahi*Bhi + Ahi*Blo + Alo*Bhi.  K is accumulated in TMEM chunks of
+// D += Ahi*Bhi + Ahi*Blo + Alo*Bhi (single-CTA tiles with BN <= 96: Ahi*[Bhi | Blo] as one
+// N = 2*BN MMA plus Alo*Bhi into the lo half, summed by the drain).  K is accumulated in TMEM chunks of
 // `drain` K blocks into two ping-ponged slots and each finished chunk is
 // drained into fp32 round-to-nearest register sums, bounding the tensor
 // core's truncating accumulation error for any K.
@@ -57,14 +58,17 @@
 // Warp roles:
 //   warps 0-3        split: for every stage, lo = x - trunc(x) beside each raw
 //                    operand the TMA loaded (elementwise on the tile image).
-//   warps 4..4+4DG-1 drain + epilogue (DG = 1, or 2 column halves for BN > 128):
+//   warps 4..4+4DG-1 drain + epilogue (DG = 1, or 2 column halves):
 //                    tcgen05.ld finished chunks, fp32 sums, + bias, ReLU,
-//                    NCHW stores (or split-K partials + deterministic reduce).
-//   next warp        TMEM allocation; one lane issues 12 tcgen05.mma per K block.
-//   last warp        one lane issues the TMA / bulk loads.
+//                    NCHW stores (or split-K partials + deterministic reduce
+//                    behind one acq_rel ticket).
+//   next warp        TMEM allocation; one lane issues the tcgen05.mma (12 per
+//                    32-wide K block, 8 with the fused issue).
+//   last warp(s)     one lane each issues the pixel TMA / the filter loads.
 // Launched with programmatic dependent launch: the prologue (barrier init,
-// TMEM alloc, tensor-map prefetch) overlaps the previous kernel;
-// griddepcontrol.wait precedes every global access.
+// TMEM alloc, tensor-map prefetch, the loaders' first-unit decode) overlaps the
+// previous kernel; griddepcontrol.wait precedes every global access.  The role
+// dispatch lists the loaders first so that their code follows the prologue.
 #pragma once
 #include <cuda.h>
 
