@@ -69,7 +69,7 @@ int main() {
     cudaMemset(d, 0, (size_t)rows * cols * 4);
     long long* cyc = nullptr;
     cudaMalloc(&cyc, 1024 * sizeof(long long));
-    struct Cfg { int mode, bw, bh; CUtensorMapSwizzle sw; const char* name; };
+    struct Cfg { int mode, bw, bh; CUtensorMapSwizzle sw; const char* name; int stride = 0; };  // stride: row pitch in bytes (0: dense)
     std::vector<Cfg> cfgs = {
         {0, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x128 SW128 (16 KB)"},
         {0, 32, 256, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x256 SW128 (32 KB)"},
@@ -79,12 +79,20 @@ int main() {
         {0, 4, 256, CU_TENSOR_MAP_SWIZZLE_NONE, "box 4x256 none (4 KB, 16 B rows)"},
         {1, 32, 128, CU_TENSOR_MAP_SWIZZLE_NONE, "bulk 16 KB"},
         {1, 32, 256, CU_TENSOR_MAP_SWIZZLE_NONE, "bulk 32 KB"},
+        // first-layer x-window rows: 128-byte rows whose starts advance by less than 128 B (overlapping,
+        // mostly unaligned), as k_tconv MODE 4 reads them for stride-2 / stride-4 convs
+        {0, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x128 SW128 pitch 128 B", 128},
+        {0, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x128 SW128 pitch 64 B", 64},
+        {0, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x128 SW128 pitch 32 B", 32},
+        {0, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, "box 32x128 SW128 pitch 48 B", 48},
     };
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     for (auto& c : cfgs) {
         CUtensorMap tm;
-        const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-        const cuuint64_t str[1] = {(cuuint64_t)cols * 4};
+        const int ccols = c.stride ? c.bw : cols;  // pitched maps: one tile column
+        const long long crows = c.stride ? ((long long)rows * cols * 4 - 512) / c.stride : rows;
+        const cuuint64_t dims[2] = {(cuuint64_t)ccols, (cuuint64_t)crows};
+        const cuuint64_t str[1] = {(cuuint64_t)(c.stride ? c.stride : cols * 4)};
         const cuuint32_t box[2] = {(cuuint32_t)c.bw, (cuuint32_t)c.bh};
         const cuuint32_t es[2] = {1, 1};
         if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, c.sw,
@@ -96,12 +104,12 @@ int main() {
         const int smem = 2048 + STAGES * bytes;
         for (int l2 = 0; l2 < 2; ++l2)
         for (int grid : {1, 16, 148}) {
-            const long long total_tiles = (long long)rows * cols * 4 / bytes;
+            const long long total_tiles = c.stride ? crows / c.bh : (long long)rows * cols * 4 / bytes;
             int iters = (int)std::min<long long>(total_tiles / grid, 2048);
             // l2: re-read a 32 MB window (L2-resident after the first pass)
             const int wrap = l2 ? (int)((32ll << 20) / bytes) : (int)total_tiles;
             if (l2) iters = 512;
-            for (int rep = 0; rep < 2; ++rep) probe<<<grid, 32, smem>>>(tm, d, c.mode, c.bw, c.bh, cols, iters, wrap, cyc);
+            for (int rep = 0; rep < 2; ++rep) probe<<<grid, 32, smem>>>(tm, d, c.mode, c.bw, c.bh, ccols, iters, wrap, cyc);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
             std::vector<long long> h(grid);
