@@ -55,6 +55,37 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, const float* base,
     cycles[blockIdx.x] = clock64() - t0;
 }
 
+// W issuing warps per CTA (lane 0 of each), each with its own STAGES-deep ring: does a second
+// issuer double the per-SM box rate (issue-bound) or not (engine / latency-bound)?
+__global__ void probe_multi(const __grid_constant__ CUtensorMap tm, int bw, int bh, int cols, int iters, int wrap_tiles,
+                            int nw, long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    const uint32_t bytes = (uint32_t)bw * bh * 4;
+    const uint32_t tiles = (smem_u32(smem) + 1024 + 1023) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES * nw; ++s) mbar_init(smem_u32(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (lane != 0 || warp >= nw) return;
+    const int tiles_x = cols / bw;
+    long long t0 = clock64();
+    for (int it = 0; it < iters + STAGES; ++it) {
+        const int s = warp * STAGES + it % STAGES;
+        if (it >= STAGES) mbar_wait(smem_u32(&bars[s]), ((it / STAGES) - 1) & 1);
+        if (it < iters) {
+            const uint32_t bar = smem_u32(&bars[s]);
+            expect_tx(bar, bytes);
+            const int t = ((blockIdx.x * nw + warp) * iters + it) % wrap_tiles;
+            tma2d(tiles + s * bytes, &tm, bar, (t % tiles_x) * bw, (t / tiles_x) * bh);
+        }
+    }
+    const long long dt = clock64() - t0;
+    atomicMax((unsigned long long*)&cycles[blockIdx.x], (unsigned long long)dt);
+}
+
 using EncFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -118,6 +149,37 @@ int main() {
             for (auto v : h) mx = v > mx ? v : mx;
             printf("%-34s %s grid %3d: %6.1f B/clk/SM  (%d tiles/CTA, %lld cyc)\n", c.name, l2 ? "L2  " : "DRAM", grid,
                    (double)iters * bytes / mx, iters, mx);
+        }
+    }
+    // issue-rate test: 16 KB SW128 boxes re-read from L2, 1 / 2 / 4 issuing warps per CTA (each a 6-deep ring)
+    {
+        CUtensorMap tm;
+        const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        const cuuint64_t str[1] = {(cuuint64_t)cols * 4};
+        const cuuint32_t box[2] = {32, 128};
+        const cuuint32_t es[2] = {1, 1};
+        enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const int bytes = 32 * 128 * 4;
+        cudaFuncSetAttribute(probe_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        for (int nw : {1, 2}) {
+            for (int grid : {1, 148}) {
+                const int iters = 256;
+                const int smem = 2048 + STAGES * nw * bytes;
+                cudaMemset(cyc, 0, 1024 * sizeof(long long));
+                for (int rep = 0; rep < 2; ++rep) {
+                    cudaMemset(cyc, 0, 1024 * sizeof(long long));
+                    probe_multi<<<grid, 32 * nw, smem>>>(tm, 32, 128, cols, iters, (int)((32ll << 20) / bytes), nw, cyc);
+                }
+                cudaError_t e = cudaDeviceSynchronize();
+                if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+                std::vector<long long> h(grid);
+                cudaMemcpy(h.data(), cyc, grid * 8, cudaMemcpyDeviceToHost);
+                long long mx = 0;
+                for (auto v : h) mx = v > mx ? v : mx;
+                printf("issuers %d grid %3d: %6.1f B/clk/SM, %.0f cycles per box per SM\n", nw, grid,
+                       (double)iters * nw * bytes / mx, (double)mx / (iters * nw));
+            }
         }
     }
     return 0;
