@@ -89,7 +89,7 @@ Geom make_geom(const b2c_conv_desc* d) {
     return g;
 }
 
-bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 96 || bn == 128 || bn == 192; }
+bool valid_bn(int bn) { return bn == 16 || bn == 32 || bn == 64 || bn == 96 || bn == 128 || bn == 192; }
 
 // K order of the tcgen05 kernels: tap-major (3) when there are >= 32 input
 // channels, flat (0) for first layers, flat contiguous (2) for conv_fc.
@@ -247,7 +247,10 @@ int applies_impl(const b2c_conv_desc* d, const b2c_tune* t, std::string& why) {
             return B2C_BAD_ARGS;
     }
     // tcgen05 family
-    if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 32,64,96,128,192"; return B2C_INAPPLICABLE; }
+    if (!valid_bn(t->tile_n)) { why = "tile_n must be one of 16,32,64,96,128,192"; return B2C_INAPPLICABLE; }
+    if (t->tile_n == 16 && !(t->variant == B2C_VAR_FC && t->swap_ab && t->tma && t->cluster <= 1)) {
+        why = "tile_n 16: the swapped TMA fc tile (conv_fc, swap_ab, tma, single CTAs)"; return B2C_INAPPLICABLE;
+    }
     if (t->split_k < 0 || (t->split_k == 0 && !t->tma)) { why = "split_k must be >= 1 (0 = stream-K, TMA kernel only)"; return B2C_BAD_ARGS; }
     if (t->cluster < 0 || t->cluster > 4) { why = "cluster must be 0..4"; return B2C_BAD_ARGS; }
     if (t->cluster == 4) {  // split-K over a thread-block cluster, fixup through DSMEM
@@ -1098,7 +1101,7 @@ int fwd_impl(const b2c_conv_desc* d, const b2c_tune* t, const float* x, const fl
         default: {
             const UmmaPlan p = umma_plan(d, t);
             UmmaEntry e = umma_pick(t->tile_n, t->swap_ab, p.kmode);
-            if (!e.fn) return fail(B2C_INAPPLICABLE, "no tcgen05 kernel for this tile");
+            if (!e.fn && !t->tma) return fail(B2C_INAPPLICABLE, "no tcgen05 kernel for this tile");  // (TMA tiles: tma_fwd picks)
             if (p.ws_bytes > 0 && (!ws || ws_bytes < p.ws_bytes))
                 return fail(B2C_BAD_ARGS, "workspace too small (see b2c_conv_workspace)");
             if (!t->prepared) {

@@ -111,7 +111,8 @@ struct TmaCfg {
     static constexpr bool CSPLIT = CL == 4;  // the split-K CTAs of a tile form one cluster; fixup over DSMEM
     static constexpr int STG_BYTES = CSPLIT ? TM_M * BN * 4 : 0;  // this CTA's partial, [col][row] fp32
     static_assert(!PAIR || (BN >= 64 && BN <= 192), "2-SM UMMA: N = BN in [64, 192] (two accumulators + A slots in TMEM)");
-    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: multiple of 32 in [32, 256]");
+    static_assert((BN % 32 == 0 && BN >= 32 && BN <= 256) || (BN == 16 && SWAP && MODE == 1),
+                  "BN: multiple of 32 in [32, 256] (16: the swapped fc tile for small batches)");
     static_assert(OCC == 1 || (OCC == 2 && BN <= 64), "two CTAs per SM: BN <= 64 (256 TMEM columns each)");
     // drain warp groups (column halves); two groups halve the exposed epilogue
     static constexpr int DG = (OCC == 1 && (BN >= 64 || SWAP)) ? 2 : 1;

@@ -78,6 +78,9 @@ TconvEntry tconv_pick_bn(int bn, int occ, int cl) {
         }
         return TconvEntry{nullptr, 0, 0};
     }
+    if constexpr (SWAP && MODE == 1) {  // fc weights on M, a 16-image pixel tile (batch <= 16)
+        if (bn == 16 && cl == 1) return occ == 2 ? tconv_entry<16, true, 1, 2, 1>() : tconv_entry<16, true, 1, 1, 1>();
+    }
     if (occ == 2) {
         switch (bn) {
             case 32: return tconv_entry<32, SWAP, MODE, 2, 1>();

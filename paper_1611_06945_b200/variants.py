@@ -41,7 +41,7 @@ from .graphopt import VariantFormats
 STATIC = "static"
 DYNAMIC = "dynamic"
 
-UMMA_BN = (32, 64, 96, 128, 192)
+UMMA_BN = (16, 32, 64, 96, 128, 192)  # 16: the swapped fc tile (batch <= 16)
 NUM_SMS = 148
 
 
@@ -255,6 +255,8 @@ class _UmmaFamily(Variant):
         best = None
         for swap in (False, True):
             for bn in UMMA_BN:
+                if bn < 32:  # (16: a tuner-only fc tile)
+                    continue
                 tiles, waste = plan(swap, bn)
                 key = (waste, -bn)
                 if best is None or key < best[0]:

@@ -61,6 +61,8 @@ def _variant_params(g):
                     TuneParams(bn=32, swap_ab=True, split_k=0, tma=1), TuneParams(bn=64, tma=1, occ=2),
                     TuneParams(bn=32, swap_ab=True, split_k=2, tma=1, occ=2), TuneParams(bn=64, tma=1, cl=2),
                     TuneParams(bn=96, split_k=2, tma=2, cl=2), TuneParams(bn=32, tma=3), TuneParams(bn=128, tma=3),
+                    TuneParams(bn=16, swap_ab=True, split_k=2, tma=1), TuneParams(bn=16, swap_ab=True, split_k=0, tma=1),
+                    TuneParams(bn=16, swap_ab=True, split_k=4, tma=2, occ=2),
                     TuneParams(bn=64, split_k=2, tma=3), TuneParams(bn=96, split_k=0, tma=3), TuneParams(bn=64, tma=3, occ=2),
                     TuneParams(bn=32, tma=4), TuneParams(bn=128, split_k=2, tma=4), TuneParams(bn=64, split_k=0, tma=4),
                     TuneParams(bn=64, tma=4, occ=2), TuneParams(bn=64, tma=1, cl=3),
@@ -248,6 +250,34 @@ def test_fc_stream_staged_full_size(cuda, row, batch):
         got = _run_device(g, x, f, b, "conv_fc_stream", p)
         r = conv_ref.compare(got, want, tol)
         assert r.ok, (p.to_string(), r)
+
+
+@pytest.mark.parametrize("row,batch,params", [(25, 5, "BN=16,sk=8,sw=1,dr=0,tm=1"), (13, 16, "BN=16,sk=4,sw=1,dr=0,tm=2,oc=2"),
+                                              (25, 10, "BN=16,sk=0,sw=1,dr=0,tm=1"), (13, 3, "BN=16,sk=8,sw=1,dr=0,tm=1,oc=2")])
+def test_fc_swap_bn16_full_size(cuda, row, batch, params):
+    """conv_fc with the 16-image swapped tile (weights on M, N = 16): fc6 / fc7 at full size on
+    reference data (fp32 tolerance) and signed data (exact ReLU clipping)."""
+    from paper_1611_06945_b200 import corpus
+    from paper_1611_06945_b200.variants import TuneParams
+
+    op = corpus.corpus(batch)[row]
+    c = {"ksz": op.ksz, "stride": op.stride, "pad": op.pad, "out_chans": op.out_chans,
+         "in": (batch, op.in_chans, op.in_y, op.in_x)}
+    g = _graph(c, True)
+    p = TuneParams.from_string("MNt=4:4,MNb=16:16,Kb=4,vw=4,lf=1,li=1," + params)
+    for low, high in ((0.1, 1.0), (-1.0, 1.0)):
+        x, f, b = conv_ref.conv_inputs(batch, op.in_chans, op.in_y, op.in_x, op.out_chans, op.ksz,
+                                       f"fc16:{row}:{batch}:{low}", low=low, high=high)
+        got = _run_device(g, x, f, b, "conv_fc", p)
+        if low > 0:
+            r = conv_ref.compare(got, conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=True),
+                                 conv_ref.tolerance_for(op.in_chans * op.ksz ** 2))
+            assert r.ok, r
+        else:
+            pre = conv_ref.ref_conv(x, f, b, op.stride, op.pad, relu=False).astype(np.float64)
+            bound = 1e-5 * conv_ref.signed_bound(x, f, op.stride, op.pad) + 1e-6
+            assert (np.abs(got.astype(np.float64) - np.maximum(pre, 0.0)) <= bound).all()
+            assert (got[pre < -bound] == 0.0).all() and (pre < -bound).any()
 
 
 @pytest.mark.parametrize("row,batch", [(25, 1), (25, 5), (13, 5), (13, 8), (25, 3), (13, 7)])
