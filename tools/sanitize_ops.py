@@ -49,6 +49,7 @@ CASES = [
     ("k_fc_stream", (2, 16, 4, 4), (4, 1, 0, 64), "conv_fc_stream", "MNt=1:4,MNb=4:1,Kb=1,vw=1,lf=1,li=1"),
     ("k_fc_smem", (3, 16, 4, 4), (4, 1, 0, 64), "conv_fc_stream", "MNt=1:2,MNb=4:1,Kb=2,vw=1,lf=1,li=1"),
     ("k_fc_bulk", (3, 16, 8, 8), (8, 1, 0, 72), "conv_fc_stream", "MNt=1:1,MNb=8:1,Kb=3,vw=1,lf=1,li=1"),
+    ("k_tconv MODE1 fc BN=16", (5, 16, 4, 4), (4, 1, 0, 160), "conv_fc", P + "BN=16,sk=2,sw=1,dr=0,tm=1,oc=2"),
     ("k_tconv MODE0 2-SM pair", (2, 32, 12, 12), (3, 1, 1, 128), "conv_umma", P + "BN=128,sk=1,sw=0,dr=0,tm=1,cl=3"),
     ("k_tconv MODE0 2-SM pair stream-K", (2, 32, 12, 12), (3, 1, 1, 96), "conv_umma", P + "BN=96,sk=0,sw=0,dr=0,tm=1,cl=3"),
     ("k_tconv split-K cluster", (1, 64, 12, 12), (3, 1, 1, 64), "conv_umma", P + "BN=64,sk=2,sw=0,dr=0,tm=1,cl=4"),
